@@ -1,0 +1,127 @@
+/*
+ * sgwls_b200.h -- C ABI of the B200-native SG-WLS filter (arXiv 1705.01674).
+ *
+ * Drop-in boundary for the reference's filter entry points.  The reference is
+ * a plain C++ static library with no plugin/FFI layer; the
+ * two functions a caller binds are
+ *
+ *   sgwls::smooth              proj/include/sgwls/smoother.hpp:30
+ *                              (definition proj/src/smoother.cpp:113-125)
+ *   sgwls::interpolate_sparse  proj/include/sgwls/smoother.hpp:41-42
+ *                              (definition proj/src/smoother.cpp:127-163)
+ *
+ * and this header exposes them as extern "C" calls on plain pointers.  The C++
+ * shim csrc/shim/smoother_gpu.cpp re-creates the exact reference signatures on
+ * top of these calls (link-substitution for proj/src/smoother.cpp); the
+ * ctypes / cffi bindings in INTEGRATION.md bind them directly.
+ *
+ * Buffers are row-major and channel-interleaved exactly like sgwls::Image
+ * (proj/include/sgwls/image.hpp:13-27): sample (y, x, c) lives at
+ * ((y*width + x)*channels + c).  Samples are fp32 (the reference holds
+ * doubles; the shim converts).  Batched calls take `batch` images back to back.
+ *
+ * Errors: every entry returns a status; on SGWLS_B200_EINVAL the message
+ * written to `err` is the reference's sgwls::Error text verbatim (config
+ * validation proj/src/smoother.cpp:103-111, proj/src/weights.cpp:7-12; input
+ * checks proj/src/smoother.cpp:115-116,129-144; pivot failure
+ * proj/src/banded.cpp:66-68).  There is no CPU fallback: without a CUDA device
+ * every compute call returns SGWLS_B200_ECUDA.
+ */
+#ifndef SGWLS_B200_H
+#define SGWLS_B200_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGWLS_B200_OK 0
+#define SGWLS_B200_EINVAL 1       /* sgwls::Error equivalent; reference text in err */
+#define SGWLS_B200_ECUDA 2        /* CUDA runtime failure or no device */
+#define SGWLS_B200_EUNSUPPORTED 3 /* valid for the reference, outside this build's limits (r > 8, C > 4) */
+
+/* device-call flags */
+#define SGWLS_B200_SYNC 1     /* synchronize the stream and report pivot failures */
+#define SGWLS_B200_VALIDATE 2 /* interpolate_sparse: validate mask/values (synchronizes) */
+
+#define SGWLS_B200_AXIS_COLUMN 0
+#define SGWLS_B200_AXIS_ROW 1
+#define SGWLS_B200_WEIGHT_FRAC 0
+#define SGWLS_B200_WEIGHT_EXP 1
+
+/* Field-for-field mirror of sgwls::SmoothConfig (proj/include/sgwls/smoother.hpp:12-24)
+ * with sgwls::WeightParams (proj/include/sgwls/weights.hpp:14-27) flattened in. */
+typedef struct sgwls_b200_config {
+    double lambda;      /* default 900 */
+    int r;              /* default 1 */
+    int tau;            /* default 1 */
+    int iterations;     /* default 4 */
+    int first_axis;     /* SGWLS_B200_AXIS_*, default Column */
+    int threads;        /* validated like the reference (>= 1); unused on the GPU */
+    int weight_kind;    /* SGWLS_B200_WEIGHT_*, default Frac */
+    double alpha_s;     /* 1.2 */
+    double alpha_r;     /* 1.2 */
+    double sigma_s;     /* 4.0 */
+    double sigma_r;     /* 3.0 */
+    double epsilon;     /* 1e-4 */
+    double guidance_scale; /* 1.0 */
+} sgwls_b200_config;
+
+/* Reference defaults (proj/include/sgwls/smoother.hpp:12-24, weights.hpp:14-27). */
+void sgwls_b200_config_default(sgwls_b200_config* cfg);
+
+/* SmoothConfig::validate (proj/src/smoother.cpp:103-111) incl. WeightParams::validate. */
+int sgwls_b200_validate(const sgwls_b200_config* cfg, char* err, size_t errlen);
+
+/* sgwls::smooth on host buffers (synchronous).  out: width*height*channels floats. */
+int sgwls_b200_smooth(const float* target, int width, int height, int channels, const float* guidance,
+                      int guidance_channels, const sgwls_b200_config* cfg, float* out, char* err, size_t errlen);
+
+/* `batch` independent smooth calls (target i with guidance i) in one launch sequence. */
+int sgwls_b200_smooth_batch(const float* targets, const float* guidances, int batch, int width, int height,
+                            int channels, int guidance_channels, const sgwls_b200_config* cfg, float* out,
+                            char* err, size_t errlen);
+
+/* Device-pointer form, ordered on `stream` (cudaStream_t; NULL = legacy default).
+ * Asynchronous unless flags & SGWLS_B200_SYNC. */
+int sgwls_b200_smooth_device(const float* d_targets, const float* d_guidances, int batch, int width, int height,
+                             int channels, int guidance_channels, const sgwls_b200_config* cfg, float* d_out,
+                             void* stream, int flags, char* err, size_t errlen);
+
+/* sgwls::interpolate_sparse on host buffers (synchronous).  values: width*height*channels,
+ * mask: width*height (0/1), out: like values, undefined_mask: width*height or NULL. */
+int sgwls_b200_interpolate_sparse(const float* values, const float* mask, int width, int height, int channels,
+                                  const float* guidance, int guidance_channels, const sgwls_b200_config* cfg,
+                                  float* out, float* undefined_mask, char* err, size_t errlen);
+
+int sgwls_b200_interpolate_sparse_batch(const float* values, const float* masks, const float* guidances,
+                                        int batch, int width, int height, int channels, int guidance_channels,
+                                        const sgwls_b200_config* cfg, float* out, float* undefined_mask,
+                                        char* err, size_t errlen);
+
+int sgwls_b200_interpolate_sparse_device(const float* d_values, const float* d_masks, const float* d_guidances,
+                                         int batch, int width, int height, int channels, int guidance_channels,
+                                         const sgwls_b200_config* cfg, float* d_out, float* d_undefined_mask,
+                                         void* stream, int flags, char* err, size_t errlen);
+
+/* Number of kernel launches one smooth / interpolate_sparse call of this shape issues
+ * (used by the benchmark's gpu_launches accounting).  Returns -1 on invalid input. */
+int sgwls_b200_kernel_launches(int width, int height, int channels, int guidance_channels, int batch, int sparse,
+                               const sgwls_b200_config* cfg);
+
+/* Host-side pass geometry (test/diagnostic hook): bands along an axis of `extent`
+ * columns swept over `sweep` rows.  info[6] = {bands, band width m, chunks P,
+ * max chunk positions, regular centres, degenerate}; centers[0..bands) = band
+ * centres (proj/src/snake.cpp:7-19), followed by the P+1 chunk row boundaries
+ * while `cap` allows.  Returns the band count or -1. */
+int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, int* centers, int cap);
+
+/* Library version string. */
+const char* sgwls_b200_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGWLS_B200_H */

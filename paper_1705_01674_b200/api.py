@@ -1,0 +1,207 @@
+"""Python host mirror of the reference filter entry points.
+
+``smooth`` mirrors ``sgwls::smooth`` (proj/include/sgwls/smoother.hpp:30,
+proj/src/smoother.cpp:113-125) and ``interpolate_sparse`` mirrors
+``sgwls::interpolate_sparse`` (proj/include/sgwls/smoother.hpp:41-42,
+proj/src/smoother.cpp:127-163): same argument meaning, same defaults, same
+``Error`` texts.  Images are numpy arrays of shape (H, W) or (H, W, C) holding
+the row-major channel-interleaved samples of ``sgwls::Image``
+(proj/include/sgwls/image.hpp:13-27); computation is fp32 on the GPU through
+the C ABI.  The ``*_device`` forms take torch CUDA tensors and stay on the
+device (stream-ordered, no host copies).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .config import Error, SmoothConfig, SparseField
+
+
+def _as_hwc(a, name: str) -> np.ndarray:
+    a = np.asarray(a)
+    if a.ndim == 2:
+        a = a[:, :, None]
+    if a.ndim != 3:
+        raise Error(f"{name}: expected an (H, W) or (H, W, C) image")
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _check_same_size(t: np.ndarray, g: np.ndarray) -> None:
+    if t.size == 0:
+        raise Error("smooth: empty target")
+    if t.shape[:2] != g.shape[:2]:
+        raise Error("smooth: target and guidance dimensions differ")
+
+
+def smooth(target, guidance, cfg: SmoothConfig | None = None) -> np.ndarray:
+    """Edge-preserving SG-WLS smoothing of ``target`` under ``guidance``."""
+    cfg = cfg or SmoothConfig()
+    squeeze = np.asarray(target).ndim == 2
+    t = _as_hwc(target, "smooth")
+    g = _as_hwc(guidance, "smooth")
+    _check_same_size(t, g)
+    h, w, c = t.shape
+    out = np.empty_like(t)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    rc = N.lib().sgwls_b200_smooth(t.ctypes.data, w, h, c, g.ctypes.data, g.shape[2], C.byref(nc),
+                                   out.ctypes.data, err, len(err))
+    N.check(rc, err)
+    return out[:, :, 0] if squeeze else out
+
+
+def smooth_batch(targets, guidances, cfg: SmoothConfig | None = None) -> np.ndarray:
+    """``len(targets)`` independent ``smooth`` calls, (B, H, W[, C]) arrays."""
+    cfg = cfg or SmoothConfig()
+    t = np.ascontiguousarray(targets, dtype=np.float32)
+    g = np.ascontiguousarray(guidances, dtype=np.float32)
+    squeeze = t.ndim == 3
+    if squeeze:
+        t = t[..., None]
+    if g.ndim == 3:
+        g = g[..., None]
+    b, h, w, c = t.shape
+    out = np.empty_like(t)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    rc = N.lib().sgwls_b200_smooth_batch(t.ctypes.data, g.ctypes.data, b, w, h, c, g.shape[3], C.byref(nc),
+                                         out.ctypes.data, err, len(err))
+    N.check(rc, err)
+    return out[..., 0] if squeeze else out
+
+
+def interpolate_sparse(field: SparseField, guidance, cfg: SmoothConfig | None = None,
+                       return_undefined: bool = False):
+    """Guided interpolation smooth(values)/smooth(mask) (Eq. 21)."""
+    cfg = cfg or SmoothConfig()
+    squeeze = np.asarray(field.values).ndim == 2
+    v = _as_hwc(field.values, "interpolate_sparse")
+    m = np.asarray(field.mask)
+    if m.ndim == 3:
+        if m.shape[2] != 1:
+            raise Error("interpolate_sparse: mask must be single-channel")
+        m = m[:, :, 0]
+    m = np.ascontiguousarray(m, dtype=np.float32)
+    if m.shape != v.shape[:2]:
+        raise Error("interpolate_sparse: values/mask size mismatch")
+    g = _as_hwc(guidance, "interpolate_sparse")
+    if g.shape[:2] != v.shape[:2]:
+        raise Error("smooth: target and guidance dimensions differ")
+    h, w, c = v.shape
+    out = np.empty_like(v)
+    und = np.empty((h, w), dtype=np.float32)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    rc = N.lib().sgwls_b200_interpolate_sparse(v.ctypes.data, m.ctypes.data, w, h, c, g.ctypes.data, g.shape[2],
+                                               C.byref(nc), out.ctypes.data, und.ctypes.data, err, len(err))
+    N.check(rc, err)
+    res = out[:, :, 0] if squeeze else out
+    return (res, und) if return_undefined else res
+
+
+def interpolate_sparse_batch(values, masks, guidances, cfg: SmoothConfig | None = None):
+    """Batched interpolate_sparse over (B, H, W) values / masks / guidances; returns (out, undefined)."""
+    cfg = cfg or SmoothConfig()
+    v = np.ascontiguousarray(values, dtype=np.float32)
+    m = np.ascontiguousarray(masks, dtype=np.float32)
+    g = np.ascontiguousarray(guidances, dtype=np.float32)
+    b, h, w = v.shape[:3]
+    c = v.shape[3] if v.ndim == 4 else 1
+    gc = g.shape[3] if g.ndim == 4 else 1
+    out = np.empty_like(v)
+    und = np.empty((b, h, w), dtype=np.float32)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    rc = N.lib().sgwls_b200_interpolate_sparse_batch(v.ctypes.data, m.ctypes.data, g.ctypes.data, b, w, h, c, gc,
+                                                     C.byref(nc), out.ctypes.data, und.ctypes.data, err, len(err))
+    N.check(rc, err)
+    return out, und
+
+
+# ------------------------------------------------------------ device forms
+
+def _stream_ptr(stream) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _dev_dims(t, name):
+    """(B, H, W, C) of a contiguous fp32 CUDA tensor shaped (H,W), (H,W,C) or (B,H,W,C)."""
+    import torch
+
+    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise Error(f"{name}: expected a contiguous float32 CUDA tensor")
+    if t.dim() == 2:
+        return 1, t.shape[0], t.shape[1], 1
+    if t.dim() == 3:
+        return 1, t.shape[0], t.shape[1], t.shape[2]
+    if t.dim() == 4:
+        return tuple(t.shape)
+    raise Error(f"{name}: bad tensor rank")
+
+
+def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, stream=None, sync: bool = False):
+    """smooth on torch CUDA tensors, (H,W[,C]) or batched (B,H,W,C); stream-ordered."""
+    import torch
+
+    cfg = cfg or SmoothConfig()
+    b, h, w, c = _dev_dims(target, "smooth")
+    bg, hg, wg, gc = _dev_dims(guidance, "smooth")
+    if (hg, wg) != (h, w) or bg != b:
+        raise Error("smooth: target and guidance dimensions differ")
+    if out is None:
+        out = torch.empty_like(target)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    rc = N.lib().sgwls_b200_smooth_device(target.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
+                                          out.data_ptr(), _stream_ptr(stream), N.SYNC if sync else 0, err,
+                                          len(err))
+    N.check(rc, err)
+    return out
+
+
+def interpolate_sparse_device(values, masks, guidances, cfg: SmoothConfig | None = None, out=None,
+                              undefined=None, stream=None, sync: bool = False, validate: bool = False):
+    """Batched interpolate_sparse on torch CUDA tensors (B,H,W) or (B,H,W,C); stream-ordered."""
+    import torch
+
+    cfg = cfg or SmoothConfig()
+    if values.dim() == 3:
+        b, h, w = values.shape
+        c = 1
+    else:
+        b, h, w, c = values.shape
+    gc = 1 if guidances.dim() == 3 else guidances.shape[3]
+    if out is None:
+        out = torch.empty_like(values)
+    und_ptr = undefined.data_ptr() if undefined is not None else None
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    flags = (N.SYNC if sync else 0) | (N.VALIDATE if validate else 0)
+    rc = N.lib().sgwls_b200_interpolate_sparse_device(values.data_ptr(), masks.data_ptr(), guidances.data_ptr(), b,
+                                                      w, h, c, gc, C.byref(nc), out.data_ptr(), und_ptr,
+                                                      _stream_ptr(stream), flags, err, len(err))
+    N.check(rc, err)
+    return out
+
+
+def validate(cfg: SmoothConfig) -> None:
+    """SmoothConfig::validate (proj/src/smoother.cpp:103-111)."""
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    N.check(N.lib().sgwls_b200_validate(C.byref(nc), err, len(err)), err)
+
+
+def kernel_launches(width, height, channels, guidance_channels, batch, sparse, cfg: SmoothConfig) -> int:
+    nc = N.to_native(cfg)
+    return int(N.lib().sgwls_b200_kernel_launches(width, height, channels, guidance_channels, batch,
+                                                  1 if sparse else 0, C.byref(nc)))
+
+
+def version() -> str:
+    return N.lib().sgwls_b200_version().decode()

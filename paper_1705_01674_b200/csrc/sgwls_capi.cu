@@ -1,0 +1,550 @@
+// sgwls_capi.cu -- host runtime and C ABI (include/sgwls_b200.h).
+//
+// Mirrors the reference pipeline (proj/src/smoother.cpp:103-163): validate the
+// configuration with the reference's error texts, then run T directional
+// passes alternating from first_axis, each pass = K1..K4 of sgwls_kernels.cu.
+// A column pass runs on the current layout; its output is written transposed
+// so the next (row) pass is again a column pass on its own layout, and the
+// last pass writes the caller's orientation.  All device memory is
+// stream-ordered (cudaMallocAsync) so concurrent host callers on different
+// streams are independent; results are deterministic (fixed summation order,
+// no float atomics).
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/sgwls_b200.h"
+#include "sgwls_kernels.h"
+
+using namespace sgwls_b200;
+
+namespace {
+
+constexpr double kMaskFloor = 1e-8;   // proj/src/smoother.cpp:15
+constexpr int kTargetChunkPositions = 48;
+
+void put_err(char* err, size_t errlen, const std::string& msg) {
+    if (err && errlen) {
+        std::strncpy(err, msg.c_str(), errlen - 1);
+        err[errlen - 1] = '\0';
+    }
+}
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw Fail{SGWLS_B200_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                             " at " #call};                                  \
+    } while (0)
+
+// SmoothConfig::validate + WeightParams::validate, same order and texts
+// (proj/src/smoother.cpp:103-111, proj/src/weights.cpp:7-12).
+int validate_cfg(const sgwls_b200_config* c, std::string& msg) {
+    if (!c) {
+        msg = "sgwls_b200: null config";
+        return SGWLS_B200_EINVAL;
+    }
+    if (!(c->lambda >= 0.0) || !std::isfinite(c->lambda)) {
+        msg = "smooth: lambda must be finite and >= 0";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->r < 1) {
+        msg = "smooth: r must be >= 1";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->tau < 1 || c->tau > 2 * c->r + 1) {
+        msg = "smooth: tau must be in [1, 2r+1], got " + std::to_string(c->tau);
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->iterations < 1) {
+        msg = "smooth: iterations must be >= 1";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->threads < 1) {
+        msg = "smooth: threads must be >= 1";
+        return SGWLS_B200_EINVAL;
+    }
+    if (!(c->epsilon > 0.0)) {
+        msg = "weights: epsilon must be > 0";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->weight_kind == SGWLS_B200_WEIGHT_EXP && (!(c->sigma_s > 0.0) || !(c->sigma_r > 0.0))) {
+        msg = "weights: sigma_s and sigma_r must be > 0 for exponential weights";
+        return SGWLS_B200_EINVAL;
+    }
+    if (!(c->guidance_scale > 0.0)) {
+        msg = "weights: guidance_scale must be > 0";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->weight_kind != SGWLS_B200_WEIGHT_EXP && c->weight_kind != SGWLS_B200_WEIGHT_FRAC) {
+        msg = "sgwls_b200: unknown weight kind";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->first_axis != 0 && c->first_axis != 1) {
+        msg = "sgwls_b200: unknown axis";
+        return SGWLS_B200_EINVAL;
+    }
+    if (c->r > kMaxR) {
+        msg = "sgwls_b200: r > " + std::to_string(kMaxR) + " is not supported by this build";
+        return SGWLS_B200_EUNSUPPORTED;
+    }
+    return SGWLS_B200_OK;
+}
+
+int check_shape(int batch, int width, int height, int channels, int gch, std::string& msg) {
+    if (batch < 1 || width <= 0 || height <= 0 || channels <= 0) {
+        msg = "smooth: empty target";
+        return SGWLS_B200_EINVAL;
+    }
+    if (channels > 4 || gch < 1 || gch > kMaxCg) {
+        msg = "sgwls_b200: channels must be in [1, 4]";
+        return SGWLS_B200_EUNSUPPORTED;
+    }
+    return SGWLS_B200_OK;
+}
+
+// Spatial LUT and folded range constants, in double then rounded once
+// (proj/src/weights.cpp:14-22, 40-71).
+void build_weights(const sgwls_b200_config* c, WeightDev& w) {
+    std::memset(&w, 0, sizeof w);
+    w.kind = c->weight_kind;
+    w.lam = (float)c->lambda;
+    const double log2e = 1.4426950408889634;
+    w.exp_k = (float)(-(c->guidance_scale * c->guidance_scale) * log2e / (2.0 * c->sigma_r * c->sigma_r));
+    w.frac_half = (float)(c->alpha_r * 0.5);
+    w.frac_lg2s = (float)std::log2(c->guidance_scale * c->guidance_scale);
+    w.eps = (float)c->epsilon;
+    for (int d2 = 0; d2 < kLutMax; ++d2) {
+        double s;
+        if (c->weight_kind == SGWLS_B200_WEIGHT_EXP)
+            s = std::exp(-d2 / (2.0 * c->sigma_s * c->sigma_s));
+        else
+            s = 1.0 / (std::pow(std::sqrt((double)d2), c->alpha_s) + c->epsilon);
+        w.spat[d2] = (float)s;
+    }
+}
+
+struct AxisPlan {
+    PassGeom g;
+    int kmax;
+    int bx;
+    size_t rec_n, rs_n, z_n, u_n;
+};
+
+// Band geometry (proj/src/snake.cpp:7-19, 21-49) and chunking of one pass layout.
+AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
+    AxisPlan ap;
+    PassGeom& g = ap.g;
+    std::memset(&g, 0, sizeof g);
+    g.Hl = Hl;
+    g.Wl = Wl;
+    g.C = C;
+    g.Cg = Cg;
+    g.r = r;
+    g.tau = tau;
+    g.batch = batch;
+    if (Wl < 2 * r + 1) {
+        g.degenerate = 1;
+        g.nb = 1;
+        g.nreg = 0;
+        g.m = Wl;  // clipped window [0, Wl-1]
+    } else {
+        const int last = Wl - 1 - r;
+        g.nreg = (last - r) / tau + 1;
+        const int lastreg = r + tau * (g.nreg - 1);
+        g.nb = g.nreg + (lastreg != last ? 1 : 0);
+        g.m = 2 * r + 1;
+    }
+    g.n = (long long)g.m * Hl;
+    int rows = kTargetChunkPositions / g.m;
+    if (rows < 1) rows = 1;
+    const int need = (2 * r + 1 + g.m - 1) / g.m;  // chunk must hold >= 2r+1 positions
+    if (rows < need) rows = need;
+    int P = (Hl + rows - 1) / rows;
+    while (P > 1 && (long long)(Hl / P) * g.m < 2 * r + 1) --P;
+    if (P < 1) P = 1;
+    g.P = P;
+    ap.kmax = ((Hl + P - 1) / P) * g.m;
+    g.img_stride = (long long)Hl * Wl * C;
+    g.gimg_stride = (long long)Hl * Wl * Cg;
+    const long long NL = (long long)g.nb * batch;
+    ap.bx = 128;
+    while (ap.bx > 32 && (size_t)ap.bx * ap.kmax * (r + C) * 4 > 200 * 1024) ap.bx /= 2;
+    ap.rec_n = P > 1 ? (size_t)P * rec_floats(r, C) * NL : 0;
+    ap.rs_n = P > 1 ? (size_t)(P - 1) * r * rs_floats(r, C) * NL : 0;
+    ap.z_n = P > 1 ? (size_t)(P - 1) * r * C * NL : 0;
+    ap.u_n = (size_t)batch * Hl * g.nb * g.m * C;
+    return ap;
+}
+
+int kernels_per_pass(const AxisPlan& ap) { return ap.g.P > 1 ? 4 : 2; }
+
+struct DevBuf {
+    float* p = nullptr;
+    cudaStream_t st = nullptr;
+    void alloc(size_t nfloats, cudaStream_t s) {
+        st = s;
+        if (nfloats) CK(cudaMallocAsync((void**)&p, nfloats * sizeof(float), s));
+    }
+    ~DevBuf() {
+        if (p) cudaFreeAsync(p, st);
+    }
+};
+
+void init_pool_once() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ULLONG_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
+void require_device() {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+        throw Fail{SGWLS_B200_ECUDA, "sgwls_b200: no CUDA device available (there is no CPU fallback)"};
+    init_pool_once();
+}
+
+// The T-pass pipeline on device buffers (proj/src/smoother.cpp:113-125).
+// Returns after enqueueing; *d_err receives the first-pass NaN-weight report.
+void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int C, int Cg,
+                const sgwls_b200_config* cfg, float* d_out, unsigned long long* d_err, cudaStream_t st) {
+    WeightDev wd;
+    build_weights(cfg, wd);
+    const int T = cfg->iterations;
+    const int fa = cfg->first_axis;
+    const bool need0 = (fa == 0) || T >= 2;
+    const bool need1 = (fa == 1) || T >= 2;
+    AxisPlan ap0 = plan_axis(H, W, C, Cg, cfg->r, cfg->tau, batch);  // column passes
+    AxisPlan ap1 = plan_axis(W, H, C, Cg, cfg->r, cfg->tau, batch);  // row passes (transposed layout)
+    auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
+    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0;
+    if (need0) {
+        rec_n = mx(rec_n, ap0.rec_n);
+        rs_n = mx(rs_n, ap0.rs_n);
+        z_n = mx(z_n, ap0.z_n);
+        u_n = mx(u_n, ap0.u_n);
+    }
+    if (need1) {
+        rec_n = mx(rec_n, ap1.rec_n);
+        rs_n = mx(rs_n, ap1.rs_n);
+        z_n = mx(z_n, ap1.z_n);
+        u_n = mx(u_n, ap1.u_n);
+    }
+    const size_t img_n = (size_t)batch * W * H * C;
+    DevBuf rec, rs, z, U, bufA, bufB, gt;
+    rec.alloc(rec_n, st);
+    rs.alloc(rs_n, st);
+    z.alloc(z_n, st);
+    U.alloc(u_n, st);
+    const int ninter = (T > 1 ? 1 : 0) + (T > 2 ? 1 : 0) + (fa == 1 ? 1 : 0);
+    if (ninter >= 1) bufA.alloc(img_n, st);
+    if (ninter >= 2) bufB.alloc(img_n, st);
+    if (need1) {
+        gt.alloc((size_t)batch * W * H * Cg, st);
+        CK(launch_transpose(d_g, gt.p, H, W, Cg, batch, st));
+    }
+    const float* src = d_t;
+    float* pingpong[2] = {bufA.p, bufB.p};
+    int src_idx = -1;  // -1: caller's buffer, else pingpong index
+    if (fa == 1) {
+        CK(launch_transpose(d_t, pingpong[0], H, W, C, batch, st));
+        src = pingpong[0];
+        src_idx = 0;
+    }
+    for (int p = 0; p < T; ++p) {
+        const int o = (fa + p) & 1;
+        const AxisPlan& ap = o == 0 ? ap0 : ap1;
+        PassLaunch pl;
+        pl.geom = ap.g;
+        pl.bx = ap.bx;
+        pl.src = src;
+        pl.guid = o == 0 ? d_g : gt.p;
+        const bool lastp = (p == T - 1);
+        pl.transpose_out = lastp ? (o == 1) : 1;
+        float* out = d_out;
+        if (!lastp) {  // never overwrite the pass input
+            const int out_idx = (src_idx == 0) ? 1 : 0;
+            out = pingpong[out_idx];
+            src_idx = out_idx;
+        }
+        pl.out = out;
+        pl.kmax = ap.kmax;
+        pl.rec = rec.p;
+        pl.rs = rs.p;
+        pl.z = z.p;
+        pl.U = U.p;
+        pl.err = (p == 0) ? d_err : nullptr;
+        pl.w = &wd;
+        CK(launch_pass(pl, st));
+        src = out;
+    }
+}
+
+std::string pivot_message(unsigned long long key) {
+    const unsigned k0 = (unsigned)(key & 0xffffffffu);
+    return "rband_lu_factorize: non-positive pivot at row " + std::to_string(k0) + " (input not SPD)";
+}
+
+struct ErrWord {
+    unsigned long long* d = nullptr;
+    cudaStream_t st;
+    explicit ErrWord(cudaStream_t s) : st(s) {
+        CK(cudaMallocAsync((void**)&d, 2 * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(d, 0xff, sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(d + 1, 0, sizeof(unsigned long long), s));
+    }
+    ~ErrWord() {
+        if (d) cudaFreeAsync(d, st);
+    }
+};
+
+// Sparse validation in the reference's order (proj/src/smoother.cpp:129-144).
+void validate_sparse(const float* d_v, const float* d_m, int batch, long long npx, int C, cudaStream_t st) {
+    unsigned long long* status = nullptr;
+    CK(cudaMallocAsync((void**)&status, 2 * sizeof(unsigned long long), st));
+    unsigned long long h[2];
+    try {
+        for (int b = 0; b < batch; ++b) {
+            CK(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), st));
+            CK(cudaMemsetAsync(status + 1, 0, sizeof(unsigned long long), st));
+            CK(launch_validate_sparse(d_v + (size_t)b * npx * C, d_m + (size_t)b * npx, npx, C, status, st));
+            CK(cudaMemcpyAsync(h, status, sizeof h, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (h[0] != ULLONG_MAX) {
+                // which violation? read that pixel's mask
+                float mv = 0.f;
+                CK(cudaMemcpy(&mv, d_m + (size_t)b * npx + h[0], sizeof(float), cudaMemcpyDeviceToHost));
+                if (mv != 0.f && mv != 1.f) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: mask must be 0/1"};
+                throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: values nonzero outside mask"};
+            }
+            if (h[1] == 0) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
+        }
+    } catch (...) {
+        cudaFreeAsync(status, st);
+        throw;
+    }
+    cudaFreeAsync(status, st);
+}
+
+void run_sparse(const float* d_v, const float* d_m, const float* d_g, int batch, int W, int H, int C, int Cg,
+                const sgwls_b200_config* cfg, float* d_out, float* d_und, unsigned long long* d_err,
+                cudaStream_t st) {
+    const long long npx = (long long)batch * W * H;
+    DevBuf packed, res;
+    packed.alloc((size_t)npx * (C + 1), st);
+    res.alloc((size_t)npx * (C + 1), st);
+    CK(launch_pack_sparse(d_v, d_m, packed.p, npx, C, st));
+    // num = smooth(values), den = smooth(mask) share every factorization: one
+    // (C+1)-channel smooth (proj/src/smoother.cpp:146-147).
+    run_smooth(packed.p, d_g, batch, W, H, C + 1, Cg, cfg, res.p, d_err, st);
+    CK(launch_ratio(res.p, d_out, d_und, npx, C, (float)kMaskFloor, st));
+}
+
+void finish_sync(unsigned long long* d_err, cudaStream_t st) {
+    unsigned long long h = ULLONG_MAX;
+    CK(cudaMemcpyAsync(&h, d_err, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(h)};
+}
+
+template <class F>
+int guarded(char* err, size_t errlen, F&& f) {
+    try {
+        f();
+        return SGWLS_B200_OK;
+    } catch (const Fail& e) {
+        put_err(err, errlen, e.msg);
+        return e.code;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, std::string("sgwls_b200: ") + e.what());
+        return SGWLS_B200_ECUDA;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+void sgwls_b200_config_default(sgwls_b200_config* c) {
+    c->lambda = 900.0;
+    c->r = 1;
+    c->tau = 1;
+    c->iterations = 4;
+    c->first_axis = SGWLS_B200_AXIS_COLUMN;
+    c->threads = 1;
+    c->weight_kind = SGWLS_B200_WEIGHT_FRAC;
+    c->alpha_s = 1.2;
+    c->alpha_r = 1.2;
+    c->sigma_s = 4.0;
+    c->sigma_r = 3.0;
+    c->epsilon = 1e-4;
+    c->guidance_scale = 1.0;
+}
+
+int sgwls_b200_validate(const sgwls_b200_config* cfg, char* err, size_t errlen) {
+    std::string msg;
+    const int rc = validate_cfg(cfg, msg);
+    if (rc) put_err(err, errlen, msg);
+    return rc;
+}
+
+int sgwls_b200_smooth_device(const float* d_t, const float* d_g, int batch, int width, int height, int channels,
+                             int gch, const sgwls_b200_config* cfg, float* d_out, void* stream, int flags,
+                             char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(batch, width, height, channels, gch, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        cudaStream_t st = (cudaStream_t)stream;
+        ErrWord ew(st);
+        run_smooth(d_t, d_g, batch, width, height, channels, gch, cfg, d_out, ew.d, st);
+        if (flags & SGWLS_B200_SYNC) finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_smooth_batch(const float* t, const float* g, int batch, int width, int height, int channels,
+                            int gch, const sgwls_b200_config* cfg, float* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(batch, width, height, channels, gch, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        cudaStream_t st = cudaStreamPerThread;
+        const size_t nt = (size_t)batch * width * height * channels, ng = (size_t)batch * width * height * gch;
+        DevBuf dt, dg, dout;
+        dt.alloc(nt, st);
+        dg.alloc(ng, st);
+        dout.alloc(nt, st);
+        CK(cudaMemcpyAsync(dt.p, t, nt * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dg.p, g, ng * 4, cudaMemcpyHostToDevice, st));
+        ErrWord ew(st);
+        run_smooth(dt.p, dg.p, batch, width, height, channels, gch, cfg, dout.p, ew.d, st);
+        CK(cudaMemcpyAsync(out, dout.p, nt * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_smooth(const float* t, int width, int height, int channels, const float* g, int gch,
+                      const sgwls_b200_config* cfg, float* out, char* err, size_t errlen) {
+    return sgwls_b200_smooth_batch(t, g, 1, width, height, channels, gch, cfg, out, err, errlen);
+}
+
+int sgwls_b200_interpolate_sparse_device(const float* d_v, const float* d_m, const float* d_g, int batch,
+                                         int width, int height, int channels, int gch,
+                                         const sgwls_b200_config* cfg, float* d_out, float* d_und, void* stream,
+                                         int flags, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::string msg;
+        int rc = check_shape(batch, width, height, channels + 1, gch, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = validate_cfg(cfg, msg);
+        require_device();
+        cudaStream_t st = (cudaStream_t)stream;
+        if (flags & SGWLS_B200_VALIDATE) validate_sparse(d_v, d_m, batch, (long long)width * height, channels, st);
+        if (rc) throw Fail{rc, msg};
+        ErrWord ew(st);
+        run_sparse(d_v, d_m, d_g, batch, width, height, channels, gch, cfg, d_out, d_und, ew.d, st);
+        if (flags & SGWLS_B200_SYNC) finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_interpolate_sparse_batch(const float* v, const float* m, const float* g, int batch, int width,
+                                        int height, int channels, int gch, const sgwls_b200_config* cfg,
+                                        float* out, float* und, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::string msg;
+        int rc = check_shape(batch, width, height, channels + 1, gch, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        cudaStream_t st = cudaStreamPerThread;
+        const size_t npx = (size_t)batch * width * height;
+        DevBuf dv, dm, dg, dout, dund;
+        dv.alloc(npx * channels, st);
+        dm.alloc(npx, st);
+        dg.alloc(npx * gch, st);
+        dout.alloc(npx * channels, st);
+        if (und) dund.alloc(npx, st);
+        CK(cudaMemcpyAsync(dv.p, v, npx * channels * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dm.p, m, npx * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dg.p, g, npx * gch * 4, cudaMemcpyHostToDevice, st));
+        // the reference validates the field before the configuration (smooth() validates cfg)
+        validate_sparse(dv.p, dm.p, batch, (long long)width * height, channels, st);
+        rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        ErrWord ew(st);
+        run_sparse(dv.p, dm.p, dg.p, batch, width, height, channels, gch, cfg, dout.p, dund.p, ew.d, st);
+        CK(cudaMemcpyAsync(out, dout.p, npx * channels * 4, cudaMemcpyDeviceToHost, st));
+        if (und) CK(cudaMemcpyAsync(und, dund.p, npx * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_interpolate_sparse(const float* v, const float* m, int width, int height, int channels,
+                                  const float* g, int gch, const sgwls_b200_config* cfg, float* out, float* und,
+                                  char* err, size_t errlen) {
+    return sgwls_b200_interpolate_sparse_batch(v, m, g, 1, width, height, channels, gch, cfg, out, und, err,
+                                               errlen);
+}
+
+int sgwls_b200_kernel_launches(int width, int height, int channels, int gch, int batch, int sparse,
+                               const sgwls_b200_config* cfg) {
+    std::string msg;
+    const int C = channels + (sparse ? 1 : 0);
+    if (validate_cfg(cfg, msg) || check_shape(batch, width, height, C, gch, msg)) return -1;
+    const AxisPlan ap0 = plan_axis(height, width, C, gch, cfg->r, cfg->tau, batch);
+    const AxisPlan ap1 = plan_axis(width, height, C, gch, cfg->r, cfg->tau, batch);
+    const int T = cfg->iterations, fa = cfg->first_axis;
+    int n = 0;
+    if (fa == 1 || T >= 2) n += 1;  // guidance transpose
+    if (fa == 1) n += 1;            // input transpose
+    for (int p = 0; p < T; ++p) n += kernels_per_pass(((fa + p) & 1) == 0 ? ap0 : ap1);
+    if (sparse) n += 2;  // pack + ratio
+    return n;
+}
+
+int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, int* centers, int cap) {
+    if (extent < 1 || sweep < 1 || r < 1 || r > kMaxR || tau < 1 || tau > 2 * r + 1) return -1;
+    const AxisPlan ap = plan_axis(sweep, extent, 1, 1, r, tau, 1);
+    if (info) {
+        info[0] = ap.g.nb;
+        info[1] = ap.g.m;
+        info[2] = ap.g.P;
+        info[3] = ap.kmax;
+        info[4] = ap.g.nreg;
+        info[5] = ap.g.degenerate;
+    }
+    for (int b = 0; b < ap.g.nb && b < cap; ++b) centers[b] = band_center(ap.g, b);
+    if (info && cap > 0) {
+        // chunk row boundaries follow the centres when room is left
+        for (int j = 0; j <= ap.g.P && ap.g.nb + j < cap; ++j) centers[ap.g.nb + j] = chunk_row(ap.g, j);
+    }
+    return ap.g.nb;
+}
+
+const char* sgwls_b200_version(void) { return "sgwls_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

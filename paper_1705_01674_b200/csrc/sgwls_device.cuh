@@ -1,0 +1,102 @@
+// sgwls_device.cuh -- device-side building blocks of the SG-WLS pass.
+//
+// Notation.  A pass works on a row-major layout of Hl rows x Wl
+// columns x C channels in which the bands are vertical strips ("column pass";
+// a row pass runs on the transposed layout).  Band b is centred on column
+// center(b) (proj/src/snake.cpp:7-19), spans columns [lo, lo+m), and is walked
+// serpentine row by row: position p = y*m + jj, column lo + (y odd ? m-1-jj : jj)
+// (proj/src/snake.cpp:21-49).  Its 1-D WLS system (proj/src/banded.cpp:13-42)
+// has unit row sums: diag = 1 + lambda*sum(w), off-diagonals -lambda*w.
+//
+// All eliminations below are written on MAGNITUDES of the (non-positive)
+// off-diagonal entries and use the row-sum pivot
+//     alpha_k = e_k + sum(remaining off-diagonal magnitudes of row k)
+// where e is the forward-eliminated all-ones right-hand side.  Every term is
+// non-negative, so fp32 loses nothing to cancellation; the
+// recurrence is algebraically identical to the reference's r-band LU
+// (proj/src/banded.cpp:44-118) with gamma = alpha*beta (symmetric A).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace sgwls_b200 {
+
+constexpr int kMaxR = 8;
+constexpr int kMaxCg = 4;
+constexpr int kLutMax = 2 * (2 * kMaxR + 1) * (2 * kMaxR + 1) + 1;
+
+// Weight parameters, pre-folded on the host in double (proj/src/weights.cpp:14-22,63-71).
+struct WeightDev {
+    int kind;          // 0 = Frac, 1 = Exp
+    float lam;         // lambda
+    float exp_k;       // Exp: -gscale^2 * log2(e) / (2 sigma_r^2)
+    float frac_half;   // Frac: alpha_r / 2
+    float frac_lg2s;   // Frac: log2(gscale^2)
+    float eps;         // Frac: epsilon
+    float spat[kLutMax];  // spatial factor by squared 2-D distance d2
+};
+
+// Geometry of one pass in its own (possibly transposed) layout.
+struct PassGeom {
+    int Hl, Wl;        // rows (sweep) and columns (band-centre axis) of the layout
+    int C, Cg;         // target / guidance channels
+    int r, tau;
+    int nb;            // bands per image
+    int nreg;          // centres of the regular progression r, r+tau, ...
+    int degenerate;    // extent < 2r+1: single clipped band
+    int m;             // band width (2r+1, or the clipped width)
+    int P;             // chunks per band
+    int batch;         // images
+    long long n;       // positions per band = m*Hl
+    long long img_stride;   // floats per image of the target layout (Hl*Wl*C)
+    long long gimg_stride;  // floats per image of the guidance layout
+};
+
+__host__ __device__ __forceinline__ int band_center(const PassGeom& g, int b) {
+    if (g.degenerate) return (g.Wl - 1) / 2;
+    return b < g.nreg ? g.r + g.tau * b : g.Wl - 1 - g.r;
+}
+
+__host__ __device__ __forceinline__ int band_lo(const PassGeom& g, int b) {
+    const int c = band_center(g, b);
+    return c - g.r > 0 ? c - g.r : 0;
+}
+
+__host__ __device__ __forceinline__ int chunk_row(const PassGeom& g, int j) {
+    return (int)(((long long)j * g.Hl) / g.P);
+}
+
+__device__ __forceinline__ float fast_ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float fast_lg2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Eq. 2 kernels on fp32 guidance (proj/src/weights.cpp:55-71).
+__device__ __forceinline__ float guidance_weight(const WeightDev& W, float range2, int d2) {
+    const float s = W.spat[d2];
+    if (W.kind == 1) return s * fast_ex2(range2 * W.exp_k);
+    // (range*gscale)^alpha_r = exp2(alpha_r/2 * (log2(range2) + log2(gscale^2))); log2(0) = -inf -> 0
+    const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
+    return s / (pr + W.eps);
+}
+
+// Position walker: serpentine coordinate of position p = y*m + jj within a band.
+__device__ __forceinline__ int serp_col(int lo, int m, int y, int jj) {
+    return lo + ((y & 1) ? (m - 1 - jj) : jj);
+}
+
+}  // namespace sgwls_b200

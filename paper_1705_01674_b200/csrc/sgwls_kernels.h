@@ -1,0 +1,37 @@
+// Host-visible launch interface of the SG-WLS kernels (sgwls_kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "sgwls_device.cuh"
+
+namespace sgwls_b200 {
+
+struct PassLaunch {
+    PassGeom geom;
+    const float* src;   // pass input, layout geom (Hl x Wl x C per image)
+    const float* guid;  // guidance in the same orientation (Hl x Wl x Cg per image)
+    float* out;         // pass output (next orientation if transpose_out)
+    int transpose_out;
+    int kmax;           // max positions of a chunk (K3 shared-memory sizing)
+    int bx;             // threads per block for K1/K3
+    float* rec;         // K1 -> K2 records
+    float* rs;          // K2 back-substitution scratch
+    float* z;           // separator values
+    float* U;           // band solutions
+    unsigned long long* err;  // NaN-weight report (first pass only), or nullptr
+    const WeightDev* w;
+};
+
+cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);
+size_t rec_floats(int r, int C);
+size_t rs_floats(int r, int C);
+cudaError_t launch_transpose(const float* in, float* out, int H, int W, int C, int batch, cudaStream_t st);
+cudaError_t launch_pack_sparse(const float* values, const float* mask, float* packed, long long npx, int C,
+                               cudaStream_t st);
+cudaError_t launch_ratio(const float* packed, float* out, float* und, long long npx, int C, float floor_,
+                         cudaStream_t st);
+cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C,
+                                   unsigned long long* status, cudaStream_t st);
+
+}  // namespace sgwls_b200
