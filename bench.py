@@ -1,0 +1,409 @@
+#!/usr/bin/env python
+"""SG-WLS filter benchmark (BASELINE.json metric: MPix/s per full filter and %
+of the HBM roofline).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c2] [--impl reference]
+
+One step = one full SG-WLS filter (all T directional passes) of one workload
+item: one image (c1/c2/c3/c5) or this rank's share of the 64-pair batch (c4).
+Default workload = BASELINE.json configs[1] (c2, the config the metric is
+quoted on that fits one GPU; configs[0] is the reference's own CPU case).
+
+* value      -- whole-job MPix/s, inputs resident in HBM, L2 flushed (256 MiB
+                memset) between timed steps, CUDA events per step on the
+                launching stream, max over ranks.
+* e2e        -- same metric through the public host-pointer C ABI
+                (sgwls_b200_smooth / _interpolate_sparse_batch) from pinned host
+                buffers: H2D of the inputs and D2H of the result every step.
+* roofline   -- one pass (K1..K4) as the unit: algorithmic bytes of a pass
+                (4*M*N*(2C+G) per image) / mean pass duration,
+                measured live with the library's per-launch CUDA events;
+                peak = MEASURED_PEAKS.json hbm_gbs.
+* cpu_baseline -- the reference library (oracle/_ref, kind "reference") or the
+                C restatement (kind "port") on the host cores, rank 0, N=1.
+* --impl reference -- the reference CPU implementation alone on this config.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1705_01674_b200 import workloads as WL  # noqa: E402
+
+METRIC = "MPix/s per full SG-WLS filter (all τ sweeps) and % of HBM roofline, 1/2/4/8 GPU"
+DATA = "synthetic: seeded Voronoi maps per BASELINE.json config text (SURVEY.md §8(d) generator), fp32 in HBM"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=10)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--secondary", action="store_true", help="iterations = tau, tau = 1 reading")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline sample budget")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def config_block(wl: WL.Workload, n: int, batch_per_rank: int) -> dict:
+    c = wl.cfg
+    return {
+        "workload": f"{wl.name}: {wl.width}x{wl.height}x{wl.channels}"
+                    + (f" x{wl.batch} pairs interpolate_sparse" if wl.sparse else "")
+                    + f", r={c.r}, tau={c.tau}, T={c.iterations}, lambda={c.lambda_:g}, range sigma={c.weight.sigma_r:g}",
+        "width": wl.width, "height": wl.height, "channels": wl.channels, "batch": wl.batch,
+        "batch_per_rank": batch_per_rank, "sparse": wl.sparse, "r": c.r, "tau": c.tau,
+        "iterations": c.iterations, "lambda": c.lambda_, "sigma_r": c.weight.sigma_r, "sigma_s": c.weight.sigma_s,
+        "weight": "exp", "guidance_scale": c.weight.guidance_scale,
+        "guidance": "luminance" if wl.name == "c2" else ("per-pair voronoi" if wl.sparse else "input"),
+        "l2": "flushed between timed steps (256 MiB memset)",
+        "parallelism": ("batch-shard" if wl.sparse else "replicas") + f" x{n}",
+    }
+
+
+# --------------------------------------------------------------- clocks
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        busy = [s for s in sm if s > 500] or sm
+        return {"sm_mhz": statistics.median(busy) if busy else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU legs
+
+def cpu_time_filter(wl: WL.Workload, inputs, kind: str, budget_s: float, max_runs: int | None = None):
+    """Time full filters of the workload on the host CPU (all cores); returns (MPix/s, runs, seconds, cores, kind)."""
+    from oracle.pyoracle import CpuOracle, available
+
+    if kind == "reference" and not available("reference"):
+        kind = "port"
+    orc = CpuOracle(kind)
+    cores = os.cpu_count() or 1
+    cfg = wl.cfg.copy(threads=cores)
+    runs, t0 = 0, time.perf_counter()
+    px = 0
+    while True:
+        if wl.sparse:
+            v, m, g = inputs[runs % len(inputs)]
+            orc.interpolate_sparse(v, m, g, cfg)
+            px += wl.width * wl.height
+        else:
+            t, g = inputs
+            orc.smooth(t, g, cfg)
+            px += wl.width * wl.height
+        runs += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or (max_runs is not None and runs >= max_runs):
+            break
+    return px / el / 1e6, runs, el, cores, kind
+
+
+# ------------------------------------------------------------------ main
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = WL.workload(args.config, secondary=args.secondary)
+
+    if args.impl == "reference":
+        return reference_arm(args, wl, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_01674_b200 as S
+    from paper_1705_01674_b200 import _native as N
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    # ---- inputs for this rank
+    if wl.sparse:
+        per = max(1, wl.batch // world)
+        ids = list(range(rank * per, rank * per + per))
+        trip = [WL.gen_c4(i) for i in ids]
+        import numpy as np
+        hv = np.stack([t[0] for t in trip])
+        hm = np.stack([t[1] for t in trip])
+        hg = np.stack([t[2] for t in trip])
+        dv, dm, dg = (torch.from_numpy(a).cuda() for a in (hv, hm, hg))
+        dout = torch.empty_like(dv)
+        batch_per_rank = per
+        px_step = per * wl.width * wl.height
+        scaling = "strong"
+    else:
+        ht, hg = WL.GENERATORS[wl.name](rank)
+        dt = torch.from_numpy(ht).cuda()
+        dg = torch.from_numpy(hg).cuda()
+        dout = torch.empty_like(dt)
+        batch_per_rank = 1
+        px_step = wl.width * wl.height
+        scaling = "weak"
+    cfg = wl.cfg
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        if wl.sparse:
+            S.interpolate_sparse_device(dv, dm, dg, cfg, out=dout, stream=stream)
+        else:
+            S.smooth_device(dt, dg, cfg, out=dout, stream=stream)
+
+    # correctness gate of this very configuration (cheap, outside timing)
+    step()
+    torch.cuda.synchronize()
+    if not bool(torch.isfinite(dout).all()):
+        raise SystemExit("non-finite output")
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    N.lib().sgwls_b200_profile(1)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        ev[k][0].record(stream)
+        step()
+        ev[k][1].record(stream)
+        flush.zero_()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    N.lib().sgwls_b200_profile(0)
+    buf = C.create_string_buffer(1 << 16)
+    N.lib().sgwls_b200_profile_read(buf, len(buf))
+    prof = json.loads(buf.value.decode())
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = world * px_step * args.steps / (total_ms / 1e3) / 1e6
+
+    # ---- roofline (pass = K1..K4 as the unit)
+    peak, peak_src = peaks()
+    c_rhs = wl.channels + (1 if wl.sparse else 0)
+    pass_bytes = batch_per_rank * 4 * wl.width * wl.height * (2 * c_rhs + 1)
+    npass = prof.get("pass", {}).get("launches", 0)
+    pass_ms = prof["pass"]["ms"] / npass if npass else None
+    kern = {k: v for k, v in prof.items() if k != "pass"}
+    dominant = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
+    kern_total = sum(v["ms"] for v in kern.values()) or 1.0
+    achieved = pass_bytes / (pass_ms / 1e3) / 1e9 if pass_ms else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{wl.name}.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                traffic = json.load(f).get("dram_bytes_per_pass")
+        except Exception:
+            traffic = None
+    filter_bytes = wl.bytes_alg() * batch_per_rank // wl.batch
+    roofline = {
+        "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+        "achieved": achieved, "frac": (achieved / peak) if achieved else None,
+        "traffic": traffic,
+        "launch_unit": "one directional pass = K1 spike-forward + K2 reduced + K3 interior + K4 average",
+        "bytes_alg_per_pass": pass_bytes, "pass_ms": pass_ms,
+        "dominant_kernel": dominant,
+        "dominant_share": (kern[dominant]["ms"] / kern_total) if dominant else None,
+        "filter_bytes_alg": filter_bytes,
+        "filter_frac": filter_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
+        "frac_vs_8tbs_nameplate": (achieved / 8000.0) if achieved else None,
+    }
+    kernels = {k: {"launches_per_step": v["launches"] / args.steps, "ms_per_step": v["ms"] / args.steps,
+                   "share": v["ms"] / kern_total} for k, v in kern.items()}
+    launches = S.kernel_launches(wl.width, wl.height, wl.channels, 1, batch_per_rank, wl.sparse, cfg)
+
+    # ---- e2e through the host-pointer C ABI from pinned buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_leg(args, wl, cfg, world, rank, dist if world > 1 else None)
+
+    # ---- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        inputs = [WL.gen_c4(i) for i in range(1)] if wl.sparse else (ht, hg)
+        mpx, runs, el, cores, kind = cpu_time_filter(wl, inputs, "reference", args.cpu_seconds)
+        cpu = {"value": mpx, "unit": "MPix/s", "cores": cores, "kind": kind,
+               "sample": f"{runs} full filter(s) of one {wl.width}x{wl.height} "
+                         f"{'pair' if wl.sparse else 'image'} ({el:.1f} s), threads={cores}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": DATA,
+            "config": config_block(wl, world, batch_per_rank),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * args.steps,
+            "clocks": clocks, "kernels": kernels,
+            "step_ms_median": statistics.median(step_ms),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, wl, cfg, world, rank, dist):
+    import numpy as np
+    import torch
+
+    from paper_1705_01674_b200 import _native as N
+
+    nc = N.to_native(cfg)
+    err = N.errbuf()
+    L = N.lib()
+    steps = args.steps
+    if wl.sparse:
+        per = max(1, wl.batch // world)
+        trip = [WL.gen_c4(rank * per + i) for i in range(per)]
+        hv = torch.from_numpy(np.stack([t[0] for t in trip])).pin_memory()
+        hm = torch.from_numpy(np.stack([t[1] for t in trip])).pin_memory()
+        hg = torch.from_numpy(np.stack([t[2] for t in trip])).pin_memory()
+        ho = torch.empty_like(hv).pin_memory()
+        hu = torch.empty_like(hm).pin_memory()
+        h2d = (hv.numel() + hm.numel() + hg.numel()) * 4
+        d2h = (ho.numel() + hu.numel()) * 4
+
+        def call():
+            rc = L.sgwls_b200_interpolate_sparse_batch(hv.data_ptr(), hm.data_ptr(), hg.data_ptr(), per, wl.width,
+                                                       wl.height, 1, 1, C.byref(nc), ho.data_ptr(), hu.data_ptr(),
+                                                       err, len(err))
+            N.check(rc, err)
+        px = per * wl.width * wl.height
+    else:
+        t, g = WL.GENERATORS[wl.name](rank)
+        ht = torch.from_numpy(t).pin_memory()
+        hg = torch.from_numpy(g).pin_memory()
+        ho = torch.empty_like(ht).pin_memory()
+        c = wl.channels
+        h2d = (ht.numel() + hg.numel()) * 4
+        d2h = ho.numel() * 4
+
+        def call():
+            rc = L.sgwls_b200_smooth(ht.data_ptr(), wl.width, wl.height, c, hg.data_ptr(), 1, C.byref(nc),
+                                     ho.data_ptr(), err, len(err))
+            N.check(rc, err)
+        px = wl.width * wl.height
+    for _ in range(max(1, args.warmup)):
+        call()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        call()
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    if dist is not None:
+        tt = torch.tensor([el], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    return {"value": world * px * steps / el / 1e6, "unit": "MPix/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": el / steps * 1e3,
+            "api": "sgwls_b200_interpolate_sparse_batch" if wl.sparse else "sgwls_b200_smooth (host pointers, pinned)"}
+
+
+def reference_arm(args, wl, rank, world):
+    if rank != 0:
+        return
+    peak, _ = peaks()
+    if wl.sparse:
+        inputs = [WL.gen_c4(i) for i in range(2)]
+    else:
+        inputs = WL.GENERATORS[wl.name](0)
+    # warm-up: one filter (timed once to size the run)
+    t0 = time.perf_counter()
+    _, _, _, cores, kind = cpu_time_filter(wl, inputs, "reference", 0.0, max_runs=1)
+    est = time.perf_counter() - t0
+    budget = 150.0
+    steps = max(1, min(args.steps, int(budget / max(est, 1e-3))))
+    warm = 0 if steps * est > 60 else min(args.warmup, 1)
+    for _ in range(warm):
+        cpu_time_filter(wl, inputs, "reference", 0.0, max_runs=1)
+    mpx, runs, el, cores, kind = cpu_time_filter(wl, inputs, "reference", 1e9, max_runs=steps)
+    ms = el / runs * 1e3
+    line = {
+        "metric": METRIC, "value": mpx, "unit": "MPix/s", "n_gpus": world, "steps": runs, "warmup": 1 + warm,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": DATA, "config": config_block(wl, world, 1 if not wl.sparse else 1), "impl": "reference",
+        "cpu_baseline": {"value": mpx, "unit": "MPix/s", "cores": cores, "kind": kind,
+                         "sample": f"{runs} full filter(s) of one {wl.width}x{wl.height} "
+                                   f"{'pair' if wl.sparse else 'image'}, threads={cores}; "
+                                   f"steps capped to ~{budget:.0f} s of CPU work (requested {args.steps})"},
+        "e2e": {"value": mpx, "unit": "MPix/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "roofline": None, "gpu_launches": 0, "hbm_peak_gbs": peak,
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -117,6 +117,13 @@ int sgwls_b200_kernel_launches(int width, int height, int channels, int guidance
  * while `cap` allows.  Returns the band count or -1. */
 int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, int* centers, int cap);
 
+/* Profiling hook: when enabled, every kernel launch is bracketed by CUDA events
+ * recorded on its own stream.  profile_read synchronizes on them, writes
+ * {"<kernel>": {"launches": n, "ms": total}, ...} (plus "pass" = whole passes)
+ * into json and clears the log.  Returns the JSON length. */
+void sgwls_b200_profile(int enable);
+int sgwls_b200_profile_read(char* json, size_t len);
+
 /* Library version string. */
 const char* sgwls_b200_version(void);
 

@@ -68,6 +68,8 @@ SIGNATURES = {
     "sgwls_b200_kernel_launches": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.POINTER(NativeConfig)]),
     "sgwls_b200_describe_pass": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int]),
+    "sgwls_b200_profile": (None, [C.c_int]),
+    "sgwls_b200_profile_read": (C.c_int, [C.c_char_p, C.c_size_t]),
     "sgwls_b200_version": (C.c_char_p, []),
 }
 

@@ -527,7 +527,7 @@ int sgwls_b200_kernel_launches(int width, int height, int channels, int gch, int
 }
 
 int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, int* centers, int cap) {
-    if (extent < 1 || sweep < 1 || r < 1 || r > kMaxR || tau < 1 || tau > 2 * r + 1) return -1;
+    if (extent < 1 || sweep < 1 || r < 1 || r > kMaxR || tau < 1) return -1;
     const AxisPlan ap = plan_axis(sweep, extent, 1, 1, r, tau, 1);
     if (info) {
         info[0] = ap.g.nb;

@@ -7,6 +7,7 @@
 
 #include "sgwls_device.cuh"
 #include "sgwls_kernels.h"
+#include "sgwls_profile.h"
 
 namespace sgwls_b200 {
 
@@ -85,6 +86,7 @@ __global__ void k_validate_sparse(const float* __restrict__ values, const float*
 // =========================================================== dispatch
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st) {
+    ProfScope ps("pass", st);
     switch (pl.geom.r) {
         case 1: return launch_pass_r<1>(pl, st);
         case 2: return launch_pass_r<2>(pl, st);
@@ -103,18 +105,21 @@ size_t rs_floats(int r, int C) { return (size_t)(2 * r - 1 + C); }
 
 cudaError_t launch_transpose(const float* in, float* out, int H, int W, int C, int batch, cudaStream_t st) {
     dim3 grid((W + 31) / 32, (H + 31) / 32, batch);
+    ProfScope ps("transpose", st);
     k_transpose<<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, C, (long long)H * W * C);
     return cudaGetLastError();
 }
 
 cudaError_t launch_pack_sparse(const float* values, const float* mask, float* packed, long long npx, int C,
                                cudaStream_t st) {
+    ProfScope ps("pack_sparse", st);
     k_pack_sparse<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(values, mask, packed, npx, C);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ratio(const float* packed, float* out, float* und, long long npx, int C, float floor_,
                          cudaStream_t st) {
+    ProfScope ps("ratio", st);
     k_ratio<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(packed, out, und, npx, C, floor_);
     return cudaGetLastError();
 }

@@ -32,6 +32,7 @@
 
 #include "sgwls_device.cuh"
 #include "sgwls_kernels.h"
+#include "sgwls_profile.h"
 
 namespace sgwls_b200 {
 
@@ -707,15 +708,27 @@ inline cudaError_t launch_pass_rc(const PassLaunch& pl, cudaStream_t st) {
     const int bx = pl.bx;
     dim3 grid1((NL + bx - 1) / bx, g.P);
     if (g.P > 1) {
-        k1_spike_forward<R, C><<<grid1, bx, 0, st>>>(g, pl.src, pl.guid, pl.rec, *pl.w);
-        k2_reduced<R, C><<<(NL + 63) / 64, 64, 0, st>>>(g, pl.rec, pl.rs, pl.z);
+        {
+            ProfScope ps("k1_spike_forward", st);
+            k1_spike_forward<R, C><<<grid1, bx, 0, st>>>(g, pl.src, pl.guid, pl.rec, *pl.w);
+        }
+        {
+            ProfScope ps("k2_reduced", st);
+            k2_reduced<R, C><<<(NL + 63) / 64, 64, 0, st>>>(g, pl.rec, pl.rs, pl.z);
+        }
     }
     const size_t smem = (size_t)bx * pl.kmax * (R + C) * sizeof(float);
     cudaError_t e = cudaFuncSetAttribute(k3_interior<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    k3_interior<R, C><<<grid1, bx, smem, st>>>(g, pl.src, pl.guid, pl.z, pl.U, pl.err, *pl.w);
+    {
+        ProfScope ps("k3_interior", st);
+        k3_interior<R, C><<<grid1, bx, smem, st>>>(g, pl.src, pl.guid, pl.z, pl.U, pl.err, *pl.w);
+    }
     dim3 grid4((g.Wl + 31) / 32, (g.Hl + 31) / 32, g.batch);
-    k4_average<C><<<grid4, dim3(32, 8), 0, st>>>(g, pl.U, pl.out, pl.transpose_out);
+    {
+        ProfScope ps("k4_average", st);
+        k4_average<C><<<grid4, dim3(32, 8), 0, st>>>(g, pl.U, pl.out, pl.transpose_out);
+    }
     (void)sizeof(RL);
     return cudaGetLastError();
 }

@@ -1,0 +1,19 @@
+// Optional per-launch CUDA-event profiling (sgwls_profile.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+namespace sgwls_b200 {
+
+// Returns a record index (or -1 when profiling is off); pair with prof_end on the same stream.
+int prof_begin(const char* name, cudaStream_t st);
+void prof_end(int idx, cudaStream_t st);
+
+struct ProfScope {
+    int idx;
+    cudaStream_t st;
+    ProfScope(const char* name, cudaStream_t s) : idx(prof_begin(name, s)), st(s) {}
+    ~ProfScope() { prof_end(idx, st); }
+};
+
+}  // namespace sgwls_b200
