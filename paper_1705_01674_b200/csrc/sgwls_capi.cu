@@ -14,6 +14,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -139,8 +140,11 @@ struct AxisPlan {
     PassGeom g;
     int kmax;
     int bx;
+    int fast, step, ncta, nw, nph;
     size_t rec_n, rs_n, z_n, u_n;
 };
+
+
 
 // Band geometry (proj/src/snake.cpp:7-19, 21-49) and chunking of one pass layout.
 AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
@@ -167,7 +171,57 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         g.m = 2 * r + 1;
     }
     g.n = (long long)g.m * Hl;
-    int rows = kTargetChunkPositions / g.m;
+    g.img_stride = (long long)Hl * Wl * C;
+    g.gimg_stride = (long long)Hl * Wl * Cg;
+    const long long NL = (long long)g.nb * batch;
+    ap.fast = (!g.degenerate && r <= kTileMaxR && (Cg == 1 || Cg == 3)) ? 1 : 0;
+    ap.step = 32;
+    ap.ncta = 1;
+    ap.nw = kTileWarps;
+    ap.nph = 1;
+    ap.bx = 128;
+    if (ap.fast) {
+        // CTA-tiled path (sgwls_tile.cuh): chunks of RW rows, tiles of nw chunks x 32 bands
+        const int RW = tile_rows_per_chunk(r, C);
+        const int P = (Hl + RW - 1) / RW;
+        g.P = P;
+        ap.kmax = RW * g.m;
+        const int PS = (P + ap.nw - 1) / ap.nw;
+        // halo: widest span of bands covering one column (incl. the forced last centre)
+        int hspan = 0;
+        for (int x = 0; x < Wl; ++x) {
+            int b0 = x - 2 * r <= 0 ? 0 : (x - 2 * r + tau - 1) / tau;
+            int b1 = x / tau;
+            if (b1 > g.nreg - 1) b1 = g.nreg - 1;
+            int bmin = b0, bmax = b1;
+            if (g.nb > g.nreg && x >= Wl - 1 - 2 * r) {
+                if (b1 < b0) bmin = g.nreg;
+                bmax = g.nreg;
+            }
+            if (bmax - bmin > hspan) hspan = bmax - bmin;
+        }
+        ap.step = 32 - hspan;
+        ap.ncta = g.nb > 32 ? 1 + (g.nb - 32 + ap.step - 1) / ap.step : 1;
+        // phases: bands of one phase must have disjoint windows
+        int nph = 1;
+        for (;; ++nph) {
+            bool ok = true;
+            for (int b = 0; b + nph < g.nb && ok; ++b)
+                if (band_center(g, b + nph) - band_center(g, b) < g.m) ok = false;
+            if (ok) break;
+        }
+        ap.nph = nph;
+        ap.rec_n = PS > 1 ? (size_t)PS * rec_floats(r, C) * NL : 0;
+        ap.rs_n = PS > 1 ? (size_t)(PS - 1) * r * rs_floats(r, C) * NL : 0;
+        ap.z_n = PS > 1 ? (size_t)(PS - 1) * r * C * NL : 0;
+        ap.u_n = 0;
+        return ap;
+    }
+    static const int target_pos = [] {
+        const char* v = std::getenv("SGWLS_CHUNK_POS");  // tuning knob (positions per chunk)
+        return v ? std::atoi(v) : kTargetChunkPositions;
+    }();
+    int rows = target_pos / g.m;
     if (rows < 1) rows = 1;
     const int need = (2 * r + 1 + g.m - 1) / g.m;  // chunk must hold >= 2r+1 positions
     if (rows < need) rows = need;
@@ -176,10 +230,6 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
     if (P < 1) P = 1;
     g.P = P;
     ap.kmax = ((Hl + P - 1) / P) * g.m;
-    g.img_stride = (long long)Hl * Wl * C;
-    g.gimg_stride = (long long)Hl * Wl * Cg;
-    const long long NL = (long long)g.nb * batch;
-    ap.bx = 128;
     while (ap.bx > 32 && (size_t)ap.bx * ap.kmax * (r + C) * 4 > 200 * 1024) ap.bx /= 2;
     ap.rec_n = P > 1 ? (size_t)P * rec_floats(r, C) * NL : 0;
     ap.rs_n = P > 1 ? (size_t)(P - 1) * r * rs_floats(r, C) * NL : 0;
@@ -188,7 +238,10 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
     return ap;
 }
 
-int kernels_per_pass(const AxisPlan& ap) { return ap.g.P > 1 ? 4 : 2; }
+int kernels_per_pass(const AxisPlan& ap) {
+    if (ap.fast) return ((ap.g.P + ap.nw - 1) / ap.nw > 1 ? 2 : 0) + 1;
+    return (ap.g.P > 1 ? 2 : 0) + 2;
+}
 
 struct DevBuf {
     float* p = nullptr;
@@ -276,6 +329,11 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         PassLaunch pl;
         pl.geom = ap.g;
         pl.bx = ap.bx;
+        pl.fast = ap.fast;
+        pl.step = ap.step;
+        pl.ncta = ap.ncta;
+        pl.nw = ap.nw;
+        pl.nph = ap.nph;
         pl.src = src;
         pl.guid = o == 0 ? d_g : gt.p;
         const bool lastp = (p == T - 1);
@@ -540,7 +598,9 @@ int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, i
     for (int b = 0; b < ap.g.nb && b < cap; ++b) centers[b] = band_center(ap.g, b);
     if (info && cap > 0) {
         // chunk row boundaries follow the centres when room is left
-        for (int j = 0; j <= ap.g.P && ap.g.nb + j < cap; ++j) centers[ap.g.nb + j] = chunk_row(ap.g, j);
+        const int rw = ap.kmax / ap.g.m;  // tiled path: uniform chunks of rw rows
+        for (int j = 0; j <= ap.g.P && ap.g.nb + j < cap; ++j)
+            centers[ap.g.nb + j] = ap.fast ? (j * rw < sweep ? j * rw : sweep) : chunk_row(ap.g, j);
     }
     return ap.g.nb;
 }

@@ -67,6 +67,14 @@ __host__ __device__ __forceinline__ int chunk_row(const PassGeom& g, int j) {
     return (int)(((long long)j * g.Hl) / g.P);
 }
 
+// Rows per chunk of the CTA-tiled path: keeps a chunk's inputs and edge weights
+// at ~64 registers (sgwls_tile.cuh).
+__host__ __device__ constexpr int tile_rows_per_chunk(int R, int C) {
+    return (64 / ((2 * R + 1) * (C + R))) < 1 ? 1 : ((64 / ((2 * R + 1) * (C + R))) > 8 ? 8 : (64 / ((2 * R + 1) * (C + R))));
+}
+constexpr int kTileMaxR = 4;
+constexpr int kTileWarps = 8;
+
 __device__ __forceinline__ float fast_ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -13,6 +13,10 @@ namespace sgwls_b200 {
 
 template <int R>
 cudaError_t launch_pass_r(const PassLaunch& pl, cudaStream_t st);
+namespace tile {
+template <int R>
+cudaError_t launch_tile_r(const PassLaunch& pl, cudaStream_t st);
+}
 
 // ============================================================ small kernels
 
@@ -87,6 +91,15 @@ __global__ void k_validate_sparse(const float* __restrict__ values, const float*
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st) {
     ProfScope ps("pass", st);
+    if (pl.fast) {
+        switch (pl.geom.r) {
+            case 1: return tile::launch_tile_r<1>(pl, st);
+            case 2: return tile::launch_tile_r<2>(pl, st);
+            case 3: return tile::launch_tile_r<3>(pl, st);
+            case 4: return tile::launch_tile_r<4>(pl, st);
+            default: return cudaErrorInvalidValue;
+        }
+    }
     switch (pl.geom.r) {
         case 1: return launch_pass_r<1>(pl, st);
         case 2: return launch_pass_r<2>(pl, st);

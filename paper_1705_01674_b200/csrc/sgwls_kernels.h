@@ -15,6 +15,11 @@ struct PassLaunch {
     int transpose_out;
     int kmax;           // max positions of a chunk (K3 shared-memory sizing)
     int bx;             // threads per block for K1/K3
+    int fast;           // regular-geometry CTA-tiled path (sgwls_tile.cuh)
+    int step;           // tiled: CTA band stride (32 - halo bands)
+    int ncta;           // tiled: CTAs across the bands
+    int nw;             // tiled: chunk warps per CTA (super-chunk size)
+    int nph;            // tiled: averaging phases
     float* rec;         // K1 -> K2 records
     float* rs;          // K2 back-substitution scratch
     float* z;           // separator values

@@ -1,0 +1,926 @@
+// sgwls_tile.cuh -- CTA-tiled fast path of the SG-WLS pass (regular geometry).
+//
+// Same exact partitioned solver as sgwls_pass.cuh, reorganised around a CTA
+// tile of 32 bands (lanes) x NW consecutive row chunks (warps):
+//
+//   chunk        = RW image rows of one band (K = RW*M positions, M = 2r+1),
+//                  its inputs, edge weights and elimination window live in
+//                  registers (all RW rows are loaded up front: full MLP);
+//   super-chunk  = the NW chunks of a CTA tile.  The separators BETWEEN the
+//                  chunks of a tile are reduced inside the CTA (shared memory,
+//                  one lane per band), so only one record per super-chunk
+//                  reaches global memory and the global reduced system (K2)
+//                  is NW times shorter.
+//
+//   KA ka_tile   spike-forward of every chunk -> chunk records in smem ->
+//                lane-per-band block elimination of the NW-1 inner separators
+//                carrying the spike toward the previous super-separator ->
+//                super-chunk record (same format as a chunk record).
+//   K2 k2_fast   sequential block-tridiagonal solve over super-separators
+//                (records prefetched), -> super-separator values.
+//   KB kb_tile   re-runs the chunk spike-forward (registers), solves the tile's
+//                inner separators with the two known super-separators as
+//                boundary values, then every chunk solves its interior with
+//                known separators (state in smem, back substitution in place),
+//                and the tile averages overlapping bands into a shared output
+//                tile in a fixed phase order (deterministic) and writes it in
+//                the next pass's transposed layout with coalesced stores.
+//
+// All eliminations: magnitudes + row-sum pivots (sgwls_device.cuh).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "sgwls_device.cuh"
+#include "sgwls_kernels.h"
+#include "sgwls_profile.h"
+#include "sgwls_fast.cuh"
+
+namespace sgwls_b200 {
+namespace tile {
+
+template <int R, int C>
+struct Rec {
+    static constexpr int NOFF = R * (R - 1) / 2;
+    static constexpr int TOFF = 0;
+    static constexpr int TCROSS = TOFF + NOFF;
+    static constexpr int TE = TCROSS + R * R;
+    static constexpr int TG = TE + R;
+    static constexpr int HOFF = TG + R * C;
+    static constexpr int HE = HOFF + NOFF;
+    static constexpr int HG = HE + R;
+    static constexpr int REC = HG + R * C;
+    static constexpr int RS = (2 * R - 1) + C;
+};
+
+__host__ __device__ constexpr int rows_per_chunk(int R, int C) { return tile_rows_per_chunk(R, C); }
+
+__device__ __forceinline__ constexpr int offi(int i, int j, int R) { return i * R - i * (i + 1) / 2 + (j - i - 1); }
+
+// squared 2-D distance of the edge (q - t, q), q at in-row index jj (regular band)
+__host__ __device__ constexpr int edge_d2(int jj, int t) {
+    return jj >= t ? t * t : 1 + (t - 1 - 2 * jj) * (t - 1 - 2 * jj);
+}
+
+// ------------------------------------------------------------ chunk inputs
+
+// Inputs of one chunk in POSITION order (serpentine resolved at load time).
+template <int R, int C, int CG, int RW>
+struct ChunkIn {
+    static constexpr int M = 2 * R + 1, K = RW * M;
+    float f[K][C];
+    float w[K][R];  // w[k][t-1] = weight of edge (k - t, k)
+};
+
+template <int R, int C, int CG, int RW>
+__device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
+                                           const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
+                                           int lo, int y0, int nrows, unsigned long long* err, int line) {
+    constexpr int M = 2 * R + 1, K = RW * M;
+    float gp[K][CG];
+    float gprev[R][CG];  // positions y0*M - R .. y0*M - 1 (last R of row y0-1)
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int jj = M - R + i;
+        const int y = y0 - 1;
+        if (y >= 0) {
+            const int co = (y & 1) ? (M - 1 - jj) : jj;
+            const float* p = G + ((long long)y * g.Wl + lo + co) * CG;
+#pragma unroll
+            for (int c = 0; c < CG; ++c) gprev[i][c] = __ldg(p + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < CG; ++c) gprev[i][c] = 0.f;
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+        const int y = y0 + rr;
+        const bool valid = rr < nrows;
+        const bool odd = y & 1;
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            const int k = rr * M + jj;
+            const int co = odd ? (M - 1 - jj) : jj;
+            if (valid) {
+                const float* pf = F + ((long long)y * g.Wl + lo + co) * C;
+                const float* pg = G + ((long long)y * g.Wl + lo + co) * CG;
+#pragma unroll
+                for (int c = 0; c < C; ++c) in.f[k][c] = __ldg(pf + c);
+#pragma unroll
+                for (int c = 0; c < CG; ++c) gp[k][c] = __ldg(pg + c);
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) in.f[k][c] = 0.f;
+#pragma unroll
+                for (int c = 0; c < CG; ++c) gp[k][c] = 0.f;
+            }
+        }
+    }
+    // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int t = 1; t <= R; ++t) {
+            float r2 = 0.f;
+#pragma unroll
+            for (int c = 0; c < CG; ++c) {
+                const float other = (k - t >= 0) ? gp[k - t >= 0 ? k - t : 0][c] : gprev[(k - t + R) >= 0 ? (k - t + R) : 0][c];
+                const float d = gp[k][c] - other;
+                r2 = fmaf(d, d, r2);
+            }
+            const float wv = guidance_weight(W, r2, edge_d2(k % M, t));
+            in.w[k][t - 1] = wv;
+            if (err != nullptr && !(wv >= 0.f)) {
+                // report only real edges: both ends exist
+                const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
+                if (exists)
+                    atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)(y0 * M + k - t));
+            }
+        }
+    }
+}
+
+// ------------------------------------------------- elimination window (scalar)
+
+// Sliding window of R+1 scalar rows with spike columns toward the left separator.
+template <int R, int C, bool SPIKE>
+struct Win {
+    float e[R + 1], g[R + 1][C], A[R + 1][R + 1], Q[R + 1][SPIKE ? R : 1];
+    float he[R], hg[R][C], hoff[R][R];
+
+    __device__ __forceinline__ void clear() {
+#pragma unroll
+        for (int i = 0; i <= R; ++i) {
+            e[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = 0.f;
+#pragma unroll
+            for (int k = 0; k <= R; ++k) A[i][k] = 0.f;
+#pragma unroll
+            for (int k = 0; k < (SPIKE ? R : 1); ++k) Q[i][k] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            he[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) hg[i][c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < R; ++k) hoff[i][k] = 0.f;
+        }
+    }
+    // eliminate slot 0; returns 1/pivot and the normalised couplings cc[1..R]
+    __device__ __forceinline__ float elim(float (&cc)[R + 1], bool head) {
+        float s = e[0];
+#pragma unroll
+        for (int i = 1; i <= R; ++i) s += A[0][i];
+        if (SPIKE) {
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) s += Q[0][mm];
+        }
+        const float inv = fast_rcp(s);
+#pragma unroll
+        for (int i = 1; i <= R; ++i) cc[i] = A[0][i] * inv;
+#pragma unroll
+        for (int i = 1; i <= R; ++i) {
+            e[i] = fmaf(cc[i], e[0], e[i]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = fmaf(cc[i], g[0][c], g[i][c]);
+#pragma unroll
+            for (int k2 = i + 1; k2 <= R; ++k2) A[i][k2] = fmaf(A[0][i], cc[k2], A[i][k2]);
+            if (SPIKE) {
+#pragma unroll
+                for (int mm = 0; mm < R; ++mm) Q[i][mm] = fmaf(cc[i], Q[0][mm], Q[i][mm]);
+            }
+        }
+        if (SPIKE && head) {
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) {
+                const float d = Q[0][mm] * inv;
+                he[mm] = fmaf(d, e[0], he[mm]);
+#pragma unroll
+                for (int c = 0; c < C; ++c) hg[mm][c] = fmaf(d, g[0][c], hg[mm][c]);
+#pragma unroll
+                for (int m2 = mm + 1; m2 < R; ++m2) hoff[mm][m2] = fmaf(d, Q[0][m2], hoff[mm][m2]);
+            }
+        }
+        return inv;
+    }
+    __device__ __forceinline__ void shift() {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            e[i] = e[i + 1];
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = g[i + 1][c];
+#pragma unroll
+            for (int k2 = i + 1; k2 < R; ++k2) A[i][k2] = A[i + 1][k2 + 1];
+            if (SPIKE) {
+#pragma unroll
+                for (int mm = 0; mm < R; ++mm) Q[i][mm] = Q[i + 1][mm];
+            }
+        }
+        e[R] = 0.f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) g[R][c] = 0.f;
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            A[i][R] = 0.f;
+            if (SPIKE) Q[R][i] = 0.f;
+        }
+    }
+};
+
+// Spike-forward over one chunk: eliminates the interior, leaves sigma_j in
+// slots 0..R-1 (non-last chunk) and the head update of sigma_{j-1}; writes the
+// chunk record into `rec` (stride `rs` floats between fields).
+template <int R, int C, int CG, int RW>
+__device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
+                                                    bool last, int kv, float* rec, int rs) {
+    using RL = Rec<R, C>;
+    constexpr int K = RW * (2 * R + 1);
+    Win<R, C, true> w;
+    w.clear();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        if (k < kv) {
+            w.e[R] = 1.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) w.g[R][c] = in.f[k][c];
+#pragma unroll
+            for (int t = 1; t <= R; ++t) {
+                const float lw = lam * in.w[k][t - 1];
+                if (k - t >= 0) {
+                    w.A[R - t][R] = lw;
+                } else if (has_left) {
+                    w.Q[R][(R - t + k) >= 0 ? (R - t + k) : 0] = lw;
+                }
+            }
+            if (k >= R) {
+                float cc[R + 1];
+                w.elim(cc, has_left);
+            }
+            w.shift();
+        }
+    }
+    if (last) {
+#pragma unroll
+        for (int d = 0; d < R; ++d) {
+            float cc[R + 1];
+            w.elim(cc, has_left);
+            w.shift();
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int k2 = i + 1; k2 < R; ++k2) rec[(RL::TOFF + offi(i, k2, R)) * rs] = w.A[i][k2];
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) rec[(RL::TCROSS + i * R + mm) * rs] = w.Q[i][mm];
+            rec[(RL::TE + i) * rs] = w.e[i];
+#pragma unroll
+            for (int c = 0; c < C; ++c) rec[(RL::TG + i * C + c) * rs] = w.g[i][c];
+        }
+    }
+#pragma unroll
+    for (int mm = 0; mm < R; ++mm) {
+#pragma unroll
+        for (int m2 = mm + 1; m2 < R; ++m2) rec[(RL::HOFF + offi(mm, m2, R)) * rs] = w.hoff[mm][m2];
+        rec[(RL::HE + mm) * rs] = w.he[mm];
+#pragma unroll
+        for (int c = 0; c < C; ++c) rec[(RL::HG + mm * C + c) * rs] = w.hg[mm][c];
+    }
+}
+
+// ---------------------------------------------- block window (separator level)
+
+// Two blocks of R scalar slots (lo = 0..R-1, hi = R..2R-1) plus spike columns.
+template <int R, int C, bool SPIKE>
+struct BWin {
+    static constexpr int W2 = 2 * R;
+    float e[W2], g[W2][C], A[W2][W2], Q[W2][SPIKE ? R : 1];
+    float he[R], hg[R][C], hoff[R][R];
+
+    __device__ __forceinline__ void clear_all() {
+#pragma unroll
+        for (int i = 0; i < W2; ++i) {
+            e[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < W2; ++k) A[i][k] = 0.f;
+#pragma unroll
+            for (int k = 0; k < (SPIKE ? R : 1); ++k) Q[i][k] = 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            he[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) hg[i][c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < R; ++k) hoff[i][k] = 0.f;
+        }
+    }
+    __device__ __forceinline__ void clear_hi() {
+#pragma unroll
+        for (int i = R; i < W2; ++i) {
+            e[i] = 0.f;
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = 0.f;
+#pragma unroll
+            for (int k = 0; k < W2; ++k) {
+                A[i][k] = 0.f;
+                A[k][i] = 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < (SPIKE ? R : 1); ++k) Q[i][k] = 0.f;
+        }
+    }
+    // eliminate lo slot mm (scalar); stores the back-substitution row into bs (if non-null)
+    __device__ __forceinline__ void elim(int mm_unused, const int mm, bool head, float* bs, int bstride) {
+        (void)mm_unused;
+        float piv = e[mm];
+#pragma unroll
+        for (int i = mm + 1; i < W2; ++i) piv += A[mm][i];
+        if (SPIKE) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) piv += Q[mm][q];
+        }
+        const float inv = fast_rcp(piv);
+        float cc[W2];
+#pragma unroll
+        for (int i = mm + 1; i < W2; ++i) cc[i] = A[mm][i] * inv;
+#pragma unroll
+        for (int i = mm + 1; i < W2; ++i) {
+            e[i] = fmaf(cc[i], e[mm], e[i]);
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = fmaf(cc[i], g[mm][c], g[i][c]);
+#pragma unroll
+            for (int k = i + 1; k < W2; ++k) A[i][k] = fmaf(A[mm][i], cc[k], A[i][k]);
+            if (SPIKE) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) Q[i][q] = fmaf(cc[i], Q[mm][q], Q[i][q]);
+            }
+        }
+        if (SPIKE && head) {
+#pragma unroll
+            for (int q = 0; q < R; ++q) {
+                const float d = Q[mm][q] * inv;
+                he[q] = fmaf(d, e[mm], he[q]);
+#pragma unroll
+                for (int c = 0; c < C; ++c) hg[q][c] = fmaf(d, g[mm][c], hg[q][c]);
+#pragma unroll
+                for (int q2 = q + 1; q2 < R; ++q2) hoff[q][q2] = fmaf(d, Q[mm][q2], hoff[q][q2]);
+            }
+        }
+        if (bs) {
+#pragma unroll
+            for (int i = mm + 1; i < W2; ++i) bs[(i - mm - 1) * bstride] = cc[i];
+#pragma unroll
+            for (int c = 0; c < C; ++c) bs[(W2 - 1 + c) * bstride] = g[mm][c] * inv;
+        }
+    }
+    __device__ __forceinline__ void shift() {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            e[i] = e[i + R];
+#pragma unroll
+            for (int c = 0; c < C; ++c) g[i][c] = g[i + R][c];
+#pragma unroll
+            for (int k = i + 1; k < R; ++k) A[i][k] = A[i + R][k + R];
+            if (SPIKE) {
+#pragma unroll
+                for (int q = 0; q < R; ++q) Q[i][q] = Q[i + R][q];
+            }
+        }
+    }
+};
+
+// Enter separator block `s` (chunk s's tail + chunk s+1's head when `with_head`)
+// into the hi slots; its coupling to the previous block goes to the window
+// (prev_in_window) or to the spike columns.
+template <int R, int C, bool SPIKE>
+__device__ __forceinline__ void enter_block(BWin<R, C, SPIKE>& w, const float* tail, const float* head, int rs,
+                                            bool with_head, bool prev_in_window, bool prev_exists) {
+    using RL = Rec<R, C>;
+    w.clear_hi();
+#pragma unroll
+    for (int mm = 0; mm < R; ++mm) {
+        w.e[R + mm] = tail[(RL::TE + mm) * rs] + (with_head ? head[(RL::HE + mm) * rs] : 0.f);
+#pragma unroll
+        for (int c = 0; c < C; ++c)
+            w.g[R + mm][c] = tail[(RL::TG + mm * C + c) * rs] + (with_head ? head[(RL::HG + mm * C + c) * rs] : 0.f);
+#pragma unroll
+        for (int m2 = mm + 1; m2 < R; ++m2)
+            w.A[R + mm][R + m2] = tail[(RL::TOFF + offi(mm, m2, R)) * rs] +
+                                  (with_head ? head[(RL::HOFF + offi(mm, m2, R)) * rs] : 0.f);
+#pragma unroll
+        for (int mp = 0; mp < R; ++mp) {
+            const float x = prev_exists ? tail[(RL::TCROSS + mm * R + mp) * rs] : 0.f;
+            if (prev_in_window) {
+                w.A[mp][R + mm] = x;
+            } else if (SPIKE) {
+                w.Q[R + mm][mp] = x;
+            }
+        }
+    }
+}
+
+// Reduce the NW chunk records of one band (lane) to its super-chunk record.
+template <int R, int C>
+__device__ __forceinline__ void reduce_super(const float* recs, int rs, int cs, int nw, bool first_super,
+                                             bool last_super, float* out, long long os) {
+    // recs: chunk s's field f at recs[s * cs + f * rs]
+    using RL = Rec<R, C>;
+    BWin<R, C, true> w;
+    w.clear_all();
+    if (!first_super) {  // head of the tile's first chunk: update of the left super-separator
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            w.he[q] = recs[(RL::HE + q) * rs];
+#pragma unroll
+            for (int c = 0; c < C; ++c) w.hg[q][c] = recs[(RL::HG + q * C + c) * rs];
+#pragma unroll
+            for (int q2 = q + 1; q2 < R; ++q2) w.hoff[q][q2] = recs[(RL::HOFF + offi(q, q2, R)) * rs];
+        }
+    }
+    const int nblk = last_super ? nw - 1 : nw;  // separators of this tile's chunks
+    for (int s = 0; s < nblk; ++s) {
+        const float* t = recs + (long long)s * cs;
+        const float* h = recs + (long long)(s + 1) * cs;
+        const bool inner = (s < nw - 1);  // sigma_s is internal (its next chunk is in the tile)
+        enter_block<R, C, true>(w, t, h, rs, inner, s > 0, s > 0 || !first_super);
+        if (s > 0) {
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, nullptr, 0);
+        }
+        w.shift();
+    }
+    if (last_super) {  // drain the final inner separator
+        if (nblk > 0) {
+            w.clear_hi();
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, nullptr, 0);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int k2 = i + 1; k2 < R; ++k2) out[(RL::TOFF + offi(i, k2, R)) * os] = w.A[i][k2];
+#pragma unroll
+            for (int q = 0; q < R; ++q) out[(RL::TCROSS + i * R + q) * os] = w.Q[i][q];
+            out[(RL::TE + i) * os] = w.e[i];
+#pragma unroll
+            for (int c = 0; c < C; ++c) out[(RL::TG + i * C + c) * os] = w.g[i][c];
+        }
+    }
+    if (!first_super) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+#pragma unroll
+            for (int q2 = q + 1; q2 < R; ++q2) out[(RL::HOFF + offi(q, q2, R)) * os] = w.hoff[q][q2];
+            out[(RL::HE + q) * os] = w.he[q];
+#pragma unroll
+            for (int c = 0; c < C; ++c) out[(RL::HG + q * C + c) * os] = w.hg[q][c];
+        }
+    }
+}
+
+// ===================================================================== KA
+
+template <int R, int C, int CG>
+__global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __restrict__ src,
+                                               const float* __restrict__ guid, float* __restrict__ srec,
+                                               const __grid_constant__ WeightDev W) {
+    constexpr int RW = rows_per_chunk(R, C);
+    constexpr int M = 2 * R + 1;
+    using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
+    const int NL = g.nb * g.batch;
+    const int L = blockIdx.x * 32 + lane;
+    const int J = blockIdx.y;
+    const int j = J * NW + wid;
+    const int nw = min(NW, g.P - J * NW);
+    const int rs = NW * 32 + 1;  // smem record field stride
+    float* rec = sm + wid * 32 + lane;
+    if (L < NL && wid < nw) {
+        const int img = L / g.nb, b = L - img * g.nb;
+        const int lo = band_lo(g, b);
+        const int y0 = j * RW;
+        const int nrows = min(RW, g.Hl - y0);
+        ChunkIn<R, C, CG, RW> in;
+        load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows,
+                                 nullptr, L);
+        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0, j == g.P - 1, nrows * M, rec, rs);
+    }
+    __syncthreads();
+    if (wid == 0 && L < NL) {
+        const int PS = (g.P + NW - 1) / NW;
+        const long long NLl = NL;
+        reduce_super<R, C>(sm + lane, rs, 32, nw, J == 0, J == PS - 1, srec + (long long)J * RL::REC * NLl + L, NLl);
+    }
+}
+
+// ===================================================================== KB
+
+struct TileOut {
+    float* out;
+    int transpose_out;
+    int step;  // CTA band stride (32 - halo)
+    int nph;   // accumulation phases
+};
+
+__device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, int& bmax) {
+    const int r = g.r, tau = g.tau;
+    const int lo_b = x - 2 * r;
+    int b0 = lo_b <= 0 ? 0 : (lo_b + tau - 1) / tau;
+    int b1 = x / tau;
+    if (b1 > g.nreg - 1) b1 = g.nreg - 1;
+    bmin = b0;
+    bmax = b1;
+    if (g.nb > g.nreg && x >= g.Wl - 1 - 2 * r) {
+        if (b1 < b0) bmin = g.nreg;
+        bmax = g.nreg;
+    }
+}
+
+template <int R, int C, int CG>
+__global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __restrict__ src,
+                                               const float* __restrict__ guid, const float* __restrict__ zs,
+                                               const TileOut to, unsigned long long* __restrict__ err,
+                                               const __grid_constant__ WeightDev W) {
+    constexpr int RW = rows_per_chunk(R, C);
+    constexpr int M = 2 * R + 1, K = RW * M, NF = R + C;
+    using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
+    const int tid = wid * 32 + lane, NT = NW * 32;
+    const int B0 = blockIdx.x * to.step;
+    const int b = B0 + lane;
+    const int J = blockIdx.y;
+    const int img = blockIdx.z;
+    const int j = J * NW + wid;
+    const int nw = min(NW, g.P - J * NW);
+    const int PS = (g.P + NW - 1) / NW;
+    const bool active = (b < g.nb) && (wid < nw);
+    const int L = img * g.nb + b;
+    const long long NLl = (long long)g.nb * g.batch;
+    const float lam = W.lam;
+    const int Y0 = J * NW * RW;
+    const int TR = min(NW * RW, g.Hl - Y0);  // tile rows
+
+    // smem carve: [recs | zint | bsc] overlaid by [state]; then [tile]
+    const int rs = NT + 1;
+    float* recs = sm;                                    // REC x rs
+    float* zint = recs + RL::REC * rs;                   // NW x R*C x 32
+    float* bsc = zint + NW * R * C * 32;                 // (NW) x R x RS x 32 back-substitution rows
+    const int stS = NT + 1;                              // state stride
+    float* state = sm;                                   // K x NF x stS (overlays the above)
+    const int region1 = max(RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32, K * NF * stS);
+    float* tl = sm + region1;                            // output tile
+    const int bl = min(B0 + 32, g.nb) - 1;
+    const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
+    const int ncol = xb - xa + 1;
+    const int TP = TR * C + 1;                           // tile pitch (per x line)
+
+    // ---- 1. spike-forward of every chunk (records to smem)
+    ChunkIn<R, C, CG, RW> in;
+    const int y0 = j * RW;
+    const int nrows = active ? min(RW, g.Hl - y0) : 0;
+    const int lo = active ? band_lo(g, b) : 0;
+    if (active) {
+        load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
+                                 L);
+        chunk_spike_forward<R, C, CG, RW>(in, lam, j > 0, j == g.P - 1, nrows * M, recs + tid, rs);
+    }
+    __syncthreads();
+
+    // ---- 2. lane-per-band solve of the tile's inner separators with the two
+    //         known super-separators as boundary values
+    if (wid == 0 && b < g.nb) {
+        const bool has_l = J > 0, has_r = J < PS - 1;
+        float zL[R][C], zR[R][C];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                zL[q][c] = has_l ? zs[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
+                zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
+            }
+        const int nint = nw - 1;  // inner separators sigma_{J*NW + i}, i < nint
+        const float* r0 = recs + lane;
+        auto T = [&](int s) { return r0 + (long long)s * 32; };  // record of tile chunk s (field stride rs)
+        BWin<R, C, false> w;
+        w.clear_all();
+        float* bs0 = bsc + lane;  // back-substitution rows: [(i*R+mm)*RS + field]*32
+        for (int s = 0; s < nint; ++s) {
+            enter_block<R, C, false>(w, T(s), T(s + 1), rs, true, s > 0, s > 0);
+            if (s == 0 && has_l) {  // known left separator: move its coupling to the RHS
+#pragma unroll
+                for (int mm = 0; mm < R; ++mm)
+#pragma unroll
+                    for (int mp = 0; mp < R; ++mp) {
+                        const float x = T(0)[(RL::TCROSS + mm * R + mp) * rs];
+                        w.e[R + mm] += x;
+#pragma unroll
+                        for (int c = 0; c < C; ++c) w.g[R + mm][c] = fmaf(x, zL[mp][c], w.g[R + mm][c]);
+                    }
+            }
+            if (s == nint - 1 && has_r) {  // known right separator (its cross toward this block)
+                const float* tr = T(nw - 1);
+#pragma unroll
+                for (int ms = 0; ms < R; ++ms)
+#pragma unroll
+                    for (int mm = 0; mm < R; ++mm) {
+                        const float x = tr[(RL::TCROSS + ms * R + mm) * rs];
+                        w.e[R + mm] += x;
+#pragma unroll
+                        for (int c = 0; c < C; ++c) w.g[R + mm][c] = fmaf(x, zR[ms][c], w.g[R + mm][c]);
+                    }
+            }
+            if (s > 0) {
+#pragma unroll
+                for (int mm = 0; mm < R; ++mm)
+                    w.elim(0, mm, false, bs0 + ((long long)((s - 1) * R + mm) * RL::RS) * 32, 32);
+            }
+            w.shift();
+        }
+        if (nint > 0) {
+            w.clear_hi();
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm)
+                w.elim(0, mm, false, bs0 + ((long long)((nint - 1) * R + mm) * RL::RS) * 32, 32);
+        }
+        float zn[R][C];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) zn[q][c] = 0.f;
+        for (int s = nint - 1; s >= 0; --s) {
+            float zc[R][C];
+#pragma unroll
+            for (int mm = R - 1; mm >= 0; --mm) {
+                const float* o = bs0 + ((long long)(s * R + mm) * RL::RS) * 32;
+#pragma unroll
+                for (int c = 0; c < C; ++c) zc[mm][c] = o[(2 * R - 1 + c) * 32];
+#pragma unroll
+                for (int i = mm + 1; i < 2 * R; ++i) {
+                    const float ci = o[(i - mm - 1) * 32];
+#pragma unroll
+                    for (int c = 0; c < C; ++c)
+                        zc[mm][c] = fmaf(ci, (i < R) ? zc[i < R ? i : 0][c] : zn[i >= R ? i - R : 0][c], zc[mm][c]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    zint[((s * R + q) * C + c) * 32 + lane] = zc[q][c];
+                    zn[q][c] = zc[q][c];
+                }
+        }
+        // the tile's boundary separators, for the chunks that touch them
+        if (has_r) {
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) zint[(((nw - 1) * R + q) * C + c) * 32 + lane] = zR[q][c];
+        }
+        // publish the left super-separator for the tile's first chunk (slot after the bs rows)
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane] = zL[q][c];
+    }
+    __syncthreads();
+
+    // ---- 3. every chunk: interior solve with known separators
+    float zl[R][C], zr[R][C];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            zl[q][c] = 0.f;
+            zr[q][c] = 0.f;
+        }
+    const bool lastc = (j == g.P - 1);
+    if (active) {
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                if (j > 0)
+                    zl[q][c] = (wid == 0) ? bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane]
+                                          : zint[(((wid - 1) * R + q) * C + c) * 32 + lane];
+                if (!lastc) zr[q][c] = zint[((wid * R + q) * C + c) * 32 + lane];
+            }
+    }
+    __syncthreads();  // the state array overlays recs / zint / bsc
+    const int kv = nrows * M;
+    const int kend = lastc ? kv : kv - R;  // interior positions [0, kend)
+    if (active) {
+        Win<R, C, false> w;
+        w.clear();
+        float* st = state + tid;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (k < kv) {
+                const bool kq = !lastc && (k >= K - R);  // known separator position (full chunk)
+                if (!kq) {
+                    w.e[R] = 1.f;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) w.g[R][c] = in.f[k][c];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < C; ++c) st[(k * NF + R + c) * stS] = zr[(k - (K - R)) >= 0 ? k - (K - R) : 0][c];
+                }
+#pragma unroll
+                for (int t = 1; t <= R; ++t) {
+                    const bool pe = (k - t >= 0) || (j > 0);
+                    if (!pe) continue;
+                    const bool pleft = (k - t < 0);
+                    const bool pright = kq && (k - t >= K - R);
+                    if (pright) continue;
+                    const float lw = lam * in.w[k][t - 1];
+                    if (!kq && !pleft) {
+                        w.A[R - t][R] = lw;
+                    } else if (!kq && pleft) {
+                        w.e[R] += lw;
+#pragma unroll
+                        for (int c = 0; c < C; ++c)
+                            w.g[R][c] = fmaf(lw, zl[(R - t + k) >= 0 ? (R - t + k) : 0][c], w.g[R][c]);
+                    } else {
+                        w.e[R - t] += lw;
+#pragma unroll
+                        for (int c = 0; c < C; ++c)
+                            w.g[R - t][c] = fmaf(lw, zr[(k - (K - R)) >= 0 ? k - (K - R) : 0][c], w.g[R - t][c]);
+                    }
+                }
+                if (k >= R) {
+                    float cc[R + 1];
+                    const float inv = w.elim(cc, false);
+#pragma unroll
+                    for (int i = 1; i <= R; ++i) st[((k - R) * NF + i - 1) * stS] = cc[i];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) st[((k - R) * NF + R + c) * stS] = w.g[0][c] * inv;
+                }
+                w.shift();
+            }
+        }
+        if (lastc) {
+            for (int d = 0; d < R; ++d) {
+                float cc[R + 1];
+                const float inv = w.elim(cc, false);
+                const int kk = kv - R + d;
+#pragma unroll
+                for (int i = 1; i <= R; ++i) st[(kk * NF + i - 1) * stS] = cc[i];
+#pragma unroll
+                for (int c = 0; c < C; ++c) st[(kk * NF + R + c) * stS] = w.g[0][c] * inv;
+                w.shift();
+            }
+        }
+        float ur[R][C];
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int c = 0; c < C; ++c) ur[i][c] = 0.f;
+        for (int k = kend - 1; k >= 0; --k) {
+            float u[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) u[c] = st[(k * NF + R + c) * stS];
+#pragma unroll
+            for (int i = 1; i <= R; ++i) {
+                const float ci = st[(k * NF + i - 1) * stS];
+#pragma unroll
+                for (int c = 0; c < C; ++c) u[c] = fmaf(ci, ur[i - 1][c], u[c]);
+            }
+#pragma unroll
+            for (int i = R - 1; i > 0; --i)
+#pragma unroll
+                for (int c = 0; c < C; ++c) ur[i][c] = ur[i - 1][c];
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                ur[0][c] = u[c];
+                st[(k * NF + R + c) * stS] = u[c];
+            }
+        }
+    }
+    // ---- 4. averaging into the shared output tile, fixed phase order
+    for (int i = tid; i < ncol * TP; i += NT) tl[i] = 0.f;
+    __syncthreads();
+    for (int ph = 0; ph < to.nph; ++ph) {
+        if (active && (lane % to.nph) == ph) {
+            const float* st = state + tid;
+            for (int k = 0; k < kv; ++k) {
+                const int rr = k / M, jj = k - rr * M;
+                const int y = y0 + rr;
+                const int co = (y & 1) ? (M - 1 - jj) : jj;
+                float* tp = tl + (lo + co - xa) * TP + (y - Y0) * C;
+#pragma unroll
+                for (int c = 0; c < C; ++c) tp[c] += st[(k * NF + R + c) * stS];
+            }
+        }
+        __syncthreads();
+    }
+    // ---- 5. owned columns -> global, coalesced
+    float* oi = to.out + img * g.img_stride;
+    if (to.transpose_out) {
+        for (int xl = wid; xl < ncol; xl += NW) {
+            const int x = xa + xl;
+            int bmin, bmax;
+            covering(g, x, bmin, bmax);
+            const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
+            if (own != (int)blockIdx.x) continue;
+            const float inv_cnt = 1.0f / (float)(bmax - bmin + 1);
+            float* orow = oi + ((long long)x * g.Hl + Y0) * C;
+            const float* trow = tl + xl * TP;
+            for (int e2 = lane; e2 < TR * C; e2 += 32) orow[e2] = trow[e2] * inv_cnt;
+        }
+    } else {
+        for (int yl = wid; yl < TR; yl += NW) {
+            float* orow = oi + ((long long)(Y0 + yl) * g.Wl + xa) * C;
+            for (int e2 = lane; e2 < ncol * C; e2 += 32) {
+                const int xl = e2 / C, c = e2 - xl * C;
+                const int x = xa + xl;
+                int bmin, bmax;
+                covering(g, x, bmin, bmax);
+                const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
+                if (own != (int)blockIdx.x) continue;
+                orow[e2] = tl[xl * TP + yl * C + c] / (float)(bmax - bmin + 1);
+            }
+        }
+    }
+}
+
+// =========================================================== host helpers
+
+template <int R, int C>
+__host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
+    constexpr int RW = rows_per_chunk(R, C);
+    constexpr int K = RW * (2 * R + 1), NF = R + C;
+    using RL = Rec<R, C>;
+    const int NT = NW * 32;
+    const size_t r1a = (size_t)RL::REC * (NT + 1) + (size_t)NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32;
+    const size_t r1b = (size_t)K * NF * (NT + 1);
+    const size_t r1 = r1a > r1b ? r1a : r1b;
+    return (r1 + (size_t)ncol * (TR * C + 1)) * sizeof(float);
+}
+
+
+// =========================================================== launchers
+
+template <int R, int C, int CG>
+inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
+    using RL = Rec<R, C>;
+    const PassGeom& g = pl.geom;
+    const int NL = g.nb * g.batch;
+    const int NW = pl.nw;
+    const int PS = (g.P + NW - 1) / NW;
+    cudaError_t e;
+    if (PS > 1) {
+        {
+            ProfScope ps("ka_tile", st);
+            const size_t smem = (size_t)RL::REC * (NW * 32 + 1) * sizeof(float);
+            e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            ka_tile<R, C, CG><<<dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st>>>(g, pl.src, pl.guid, pl.rec, *pl.w);
+        }
+        {
+            ProfScope ps("k2_reduced", st);
+            PassGeom gs = g;
+            gs.P = PS;
+            fast::k2_fast<R, C, 4><<<(NL + 31) / 32, 32, 0, st>>>(gs, pl.rec, pl.rs, pl.z);
+        }
+    }
+    {
+        ProfScope ps("kb_tile", st);
+        constexpr int RW = rows_per_chunk(R, C);
+        const int ncol = 31 * g.tau + 2 * g.r + 1;
+        const size_t smem = kb_smem_bytes<R, C>(NW, NW * RW, ncol);
+        e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph};
+        kb_tile<R, C, CG><<<dim3(pl.ncta, PS, g.batch), dim3(32, NW), smem, st>>>(g, pl.src, pl.guid, pl.z, to,
+                                                                                 pl.err, *pl.w);
+    }
+    return cudaGetLastError();
+}
+
+template <int R, int C>
+inline cudaError_t launch_tile_rc(const PassLaunch& pl, cudaStream_t st) {
+    return pl.geom.Cg == 1 ? launch_tile_rcg<R, C, 1>(pl, st) : launch_tile_rcg<R, C, 3>(pl, st);
+}
+
+template <int R>
+cudaError_t launch_tile_r(const PassLaunch& pl, cudaStream_t st) {
+    switch (pl.geom.C) {
+        case 1: return launch_tile_rc<R, 1>(pl, st);
+        case 2: return launch_tile_rc<R, 2>(pl, st);
+        case 3: return launch_tile_rc<R, 3>(pl, st);
+        case 4: return launch_tile_rc<R, 4>(pl, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace tile
+}  // namespace sgwls_b200
