@@ -44,6 +44,8 @@ extern "C" {
 /* device-call flags */
 #define SGWLS_B200_SYNC 1     /* synchronize the stream and report pivot failures */
 #define SGWLS_B200_VALIDATE 2 /* interpolate_sparse: validate mask/values (synchronizes) */
+#define SGWLS_B200_GRAPH 4    /* capture the call into a CUDA graph once per (pointers, shape, config)
+                                 and replay it on later identical calls */
 
 #define SGWLS_B200_AXIS_COLUMN 0
 #define SGWLS_B200_AXIS_ROW 1
@@ -123,6 +125,9 @@ int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, i
  * into json and clears the log.  Returns the JSON length. */
 void sgwls_b200_profile(int enable);
 int sgwls_b200_profile_read(char* json, size_t len);
+/* Fold the recorded launch times into the running totals (synchronizes on them);
+ * call after every replay when profiling graph-replayed calls. */
+void sgwls_b200_profile_collect(void);
 
 /* Library version string. */
 const char* sgwls_b200_version(void);

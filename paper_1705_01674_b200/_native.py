@@ -14,7 +14,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "libsgwls_b200.so")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
-SYNC, VALIDATE = 1, 2
+SYNC, VALIDATE, GRAPH = 1, 2, 4
 
 
 class NativeConfig(C.Structure):
@@ -70,6 +70,7 @@ SIGNATURES = {
     "sgwls_b200_describe_pass": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, _P, _P, C.c_int]),
     "sgwls_b200_profile": (None, [C.c_int]),
     "sgwls_b200_profile_read": (C.c_int, [C.c_char_p, C.c_size_t]),
+    "sgwls_b200_profile_collect": (None, []),
     "sgwls_b200_version": (C.c_char_p, []),
 }
 

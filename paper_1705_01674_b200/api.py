@@ -145,8 +145,10 @@ def _dev_dims(t, name):
     raise Error(f"{name}: bad tensor rank")
 
 
-def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, stream=None, sync: bool = False):
-    """smooth on torch CUDA tensors, (H,W[,C]) or batched (B,H,W,C); stream-ordered."""
+def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, stream=None, sync: bool = False,
+                  graph: bool = False):
+    """smooth on torch CUDA tensors, (H,W[,C]) or batched (B,H,W,C); stream-ordered.
+    graph=True captures the call into a CUDA graph once per (buffers, shape, config) and replays it."""
     import torch
 
     cfg = cfg or SmoothConfig()
@@ -158,15 +160,16 @@ def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, s
         out = torch.empty_like(target)
     err = N.errbuf()
     nc = N.to_native(cfg)
+    flags = (N.SYNC if sync else 0) | (N.GRAPH if graph else 0)
     rc = N.lib().sgwls_b200_smooth_device(target.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
-                                          out.data_ptr(), _stream_ptr(stream), N.SYNC if sync else 0, err,
-                                          len(err))
+                                          out.data_ptr(), _stream_ptr(stream), flags, err, len(err))
     N.check(rc, err)
     return out
 
 
 def interpolate_sparse_device(values, masks, guidances, cfg: SmoothConfig | None = None, out=None,
-                              undefined=None, stream=None, sync: bool = False, validate: bool = False):
+                              undefined=None, stream=None, sync: bool = False, validate: bool = False,
+                              graph: bool = False):
     """Batched interpolate_sparse on torch CUDA tensors (B,H,W) or (B,H,W,C); stream-ordered."""
     import torch
 
@@ -182,7 +185,7 @@ def interpolate_sparse_device(values, masks, guidances, cfg: SmoothConfig | None
     und_ptr = undefined.data_ptr() if undefined is not None else None
     err = N.errbuf()
     nc = N.to_native(cfg)
-    flags = (N.SYNC if sync else 0) | (N.VALIDATE if validate else 0)
+    flags = (N.SYNC if sync else 0) | (N.VALIDATE if validate else 0) | (N.GRAPH if graph else 0)
     rc = N.lib().sgwls_b200_interpolate_sparse_device(values.data_ptr(), masks.data_ptr(), guidances.data_ptr(), b,
                                                       w, h, c, gc, C.byref(nc), out.data_ptr(), und_ptr,
                                                       _stream_ptr(stream), flags, err, len(err))

@@ -16,11 +16,14 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <memory>
 #include <mutex>
 #include <string>
 
 #include "../../include/sgwls_b200.h"
 #include "sgwls_kernels.h"
+#include "sgwls_profile.h"
 
 using namespace sgwls_b200;
 
@@ -424,6 +427,83 @@ void finish_sync(unsigned long long* d_err, cudaStream_t st) {
     if (h != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(h)};
 }
 
+
+// ------------------------------------------------------ CUDA-graph replay
+//
+// With SGWLS_B200_GRAPH the whole call (every pass, every kernel, the
+// stream-ordered scratch allocations) is captured once into a CUDA graph keyed
+// by (pointers, shape, configuration) and replayed on later calls with the
+// same key: one launch per call instead of ~4 per pass, no host gaps.  The
+// graph runs on a private stream joined to the caller's stream with events.
+struct GraphEntry {
+    cudaGraphExec_t exec = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    unsigned long long* d_err = nullptr;
+    int armed = 0;
+};
+std::mutex g_graph_mu;
+std::map<std::string, std::unique_ptr<GraphEntry>> g_graphs;
+
+std::string graph_key(const void* const* ptrs, int nptr, const int* dims, int ndims, const sgwls_b200_config* cfg,
+                      int kind) {
+    std::string k;
+    k.append((const char*)ptrs, sizeof(void*) * nptr);
+    k.append((const char*)dims, sizeof(int) * ndims);
+    k.append((const char*)cfg, sizeof(*cfg));
+    k.append((const char*)&kind, sizeof kind);
+    const int prof = prof_enabled() ? 1 : 0;
+    k.append((const char*)&prof, sizeof prof);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    k.append((const char*)&dev, sizeof dev);
+    return k;
+}
+
+template <class F>
+void run_graphed(const std::string& key, cudaStream_t user, bool sync, F&& body) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    std::unique_ptr<GraphEntry>& slot = g_graphs[key];
+    if (!slot) {
+        auto ge = std::make_unique<GraphEntry>();
+        CK(cudaStreamCreateWithFlags(&ge->st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ge->ev_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ge->ev_out, cudaEventDisableTiming));
+        CK(cudaMalloc((void**)&ge->d_err, 2 * sizeof(unsigned long long)));
+        cudaGraph_t graph = nullptr;
+        CK(cudaStreamBeginCapture(ge->st, cudaStreamCaptureModeRelaxed));
+        prof_set_capture(&ge->armed);
+        try {
+            CK(cudaMemsetAsync(ge->d_err, 0xff, sizeof(unsigned long long), ge->st));
+            body(ge->st, ge->d_err);
+        } catch (...) {
+            prof_set_capture(nullptr);
+            cudaStreamEndCapture(ge->st, &graph);
+            if (graph) cudaGraphDestroy(graph);
+            throw;
+        }
+        prof_set_capture(nullptr);
+        CK(cudaStreamEndCapture(ge->st, &graph));
+        cudaError_t ie = cudaGraphInstantiate(&ge->exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CK(ie);
+        slot = std::move(ge);
+    }
+    GraphEntry& ge = *slot;
+    CK(cudaEventRecord(ge.ev_in, user));
+    CK(cudaStreamWaitEvent(ge.st, ge.ev_in, 0));
+    CK(cudaGraphLaunch(ge.exec, ge.st));
+    ge.armed = 1;
+    CK(cudaEventRecord(ge.ev_out, ge.st));
+    CK(cudaStreamWaitEvent(user, ge.ev_out, 0));
+    if (sync) {
+        unsigned long long h = ULLONG_MAX;
+        CK(cudaMemcpyAsync(&h, ge.d_err, sizeof h, cudaMemcpyDeviceToHost, user));
+        CK(cudaStreamSynchronize(user));
+        if (h != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(h)};
+    }
+}
+
 template <class F>
 int guarded(char* err, size_t errlen, F&& f) {
     try {
@@ -476,6 +556,15 @@ int sgwls_b200_smooth_device(const float* d_t, const float* d_g, int batch, int 
         if (rc) throw Fail{rc, msg};
         require_device();
         cudaStream_t st = (cudaStream_t)stream;
+        if (flags & SGWLS_B200_GRAPH) {
+            const void* ptrs[3] = {d_t, d_g, d_out};
+            const int dims[5] = {batch, width, height, channels, gch};
+            run_graphed(graph_key(ptrs, 3, dims, 5, cfg, 0), st, flags & SGWLS_B200_SYNC,
+                        [&](cudaStream_t gs, unsigned long long* de) {
+                            run_smooth(d_t, d_g, batch, width, height, channels, gch, cfg, d_out, de, gs);
+                        });
+            return;
+        }
         ErrWord ew(st);
         run_smooth(d_t, d_g, batch, width, height, channels, gch, cfg, d_out, ew.d, st);
         if (flags & SGWLS_B200_SYNC) finish_sync(ew.d, st);
@@ -524,6 +613,15 @@ int sgwls_b200_interpolate_sparse_device(const float* d_v, const float* d_m, con
         cudaStream_t st = (cudaStream_t)stream;
         if (flags & SGWLS_B200_VALIDATE) validate_sparse(d_v, d_m, batch, (long long)width * height, channels, st);
         if (rc) throw Fail{rc, msg};
+        if (flags & SGWLS_B200_GRAPH) {
+            const void* ptrs[5] = {d_v, d_m, d_g, d_out, d_und};
+            const int dims[5] = {batch, width, height, channels, gch};
+            run_graphed(graph_key(ptrs, 5, dims, 5, cfg, 1), st, flags & SGWLS_B200_SYNC,
+                        [&](cudaStream_t gs, unsigned long long* de) {
+                            run_sparse(d_v, d_m, d_g, batch, width, height, channels, gch, cfg, d_out, d_und, de, gs);
+                        });
+            return;
+        }
         ErrWord ew(st);
         run_sparse(d_v, d_m, d_g, batch, width, height, channels, gch, cfg, d_out, d_und, ew.d, st);
         if (flags & SGWLS_B200_SYNC) finish_sync(ew.d, st);

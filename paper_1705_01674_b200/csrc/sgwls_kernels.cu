@@ -20,29 +20,26 @@ cudaError_t launch_tile_r(const PassLaunch& pl, cudaStream_t st);
 
 // ============================================================ small kernels
 
-// out[img][x][y][c] = in[img][y][x][c]  (H x W x C -> W x H x C), tiled.
-__global__ void __launch_bounds__(256) k_transpose(const float* __restrict__ in, float* __restrict__ out, int H,
-                                                   int W, int C, long long stride) {
-    __shared__ float tile[32][33 * 4];
+// out[img][x][y][c] = in[img][y][x][c]  (H x W x C -> W x H x C), 32x32 pixel
+// tiles through shared memory; both the read and the write are row-coalesced.
+template <int C>
+__global__ void __launch_bounds__(256) k_transpose(const float* __restrict__ in, float* __restrict__ out, int H, int W,
+                                                   long long stride) {
+    __shared__ float tile[32][32 * C + 1];
     const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32, img = blockIdx.z;
     const float* ii = in + img * stride;
     float* oo = out + img * stride;
-    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
-        const int y = y0 + yy;
-        for (int idx = threadIdx.x; idx < 32 * C; idx += 32) {
-            const int xx = idx / C, c = idx - xx * C;
-            const int x = x0 + xx;
-            if (y < H && x < W) tile[yy][xx * C + c] = ii[((long long)y * W + x) * C + c];
-        }
+    const int nx = min(32, W - x0), ny = min(32, H - y0);
+    for (int yy = threadIdx.y; yy < ny; yy += blockDim.y) {
+        const float* row = ii + ((long long)(y0 + yy) * W + x0) * C;
+        for (int i = threadIdx.x; i < nx * C; i += 32) tile[yy][i] = __ldg(row + i);
     }
     __syncthreads();
-    for (int xx = threadIdx.y; xx < 32; xx += blockDim.y) {
-        const int x = x0 + xx;
-        if (x >= W) continue;
-        for (int idx = threadIdx.x; idx < 32 * C; idx += 32) {
-            const int yy = idx / C, c = idx - yy * C;
-            const int y = y0 + yy;
-            if (y < H) oo[((long long)x * H + y) * C + c] = tile[yy][xx * C + c];
+    for (int xx = threadIdx.y; xx < nx; xx += blockDim.y) {
+        float* row = oo + ((long long)(x0 + xx) * H + y0) * C;
+        for (int i = threadIdx.x; i < ny * C; i += 32) {
+            const int yy = i / C, c = i - yy * C;
+            row[i] = tile[yy][xx * C + c];
         }
     }
 }
@@ -119,7 +116,14 @@ size_t rs_floats(int r, int C) { return (size_t)(2 * r - 1 + C); }
 cudaError_t launch_transpose(const float* in, float* out, int H, int W, int C, int batch, cudaStream_t st) {
     dim3 grid((W + 31) / 32, (H + 31) / 32, batch);
     ProfScope ps("transpose", st);
-    k_transpose<<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, C, (long long)H * W * C);
+    const long long stride = (long long)H * W * C;
+    switch (C) {
+        case 1: k_transpose<1><<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, stride); break;
+        case 2: k_transpose<2><<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, stride); break;
+        case 3: k_transpose<3><<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, stride); break;
+        case 4: k_transpose<4><<<grid, dim3(32, 8), 0, st>>>(in, out, H, W, stride); break;
+        default: return cudaErrorInvalidValue;
+    }
     return cudaGetLastError();
 }
 

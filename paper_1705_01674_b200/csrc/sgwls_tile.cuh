@@ -427,7 +427,7 @@ __device__ __forceinline__ void enter_block(BWin<R, C, SPIKE>& w, const float* t
 
 // Reduce the NW chunk records of one band (lane) to its super-chunk record.
 template <int R, int C>
-__device__ __forceinline__ void reduce_super(const float* recs, int rs, int cs, int nw, bool first_super,
+__device__ __forceinline__ void reduce_super(const float* recs, long long rs, long long cs, int nw, bool first_super,
                                              bool last_super, float* out, long long os) {
     // recs: chunk s's field f at recs[s * cs + f * rs]
     using RL = Rec<R, C>;
@@ -448,7 +448,7 @@ __device__ __forceinline__ void reduce_super(const float* recs, int rs, int cs, 
         const float* t = recs + (long long)s * cs;
         const float* h = recs + (long long)(s + 1) * cs;
         const bool inner = (s < nw - 1);  // sigma_s is internal (its next chunk is in the tile)
-        enter_block<R, C, true>(w, t, h, rs, inner, s > 0, s > 0 || !first_super);
+        enter_block<R, C, true>(w, t, h, (int)rs, inner, s > 0, s > 0 || !first_super);
         if (s > 0) {
 #pragma unroll
             for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, nullptr, 0);
@@ -483,6 +483,152 @@ __device__ __forceinline__ void reduce_super(const float* recs, int rs, int cs, 
             for (int c = 0; c < C; ++c) out[(RL::HG + q * C + c) * os] = w.hg[q][c];
         }
     }
+}
+
+
+// Solve the inner separators of a run of `nw` chunk records (inner separators =
+// the separators of chunks 0..nw-2) with the left / right separators known
+// (has_l: zL, has_r: zR).  Record s's field f is at recs[s*cs + f*rs]; the
+// solution of inner separator s, component (q, c) goes to
+// zout[((s*R + q)*C + c) * zst]; back-substitution rows use bs (stride bss).
+template <int R, int C>
+__device__ __forceinline__ void solve_inner(const float* recs, long long rs, long long cs, int nw, bool has_l,
+                                            const float (&zL)[R][C], bool has_r, const float (&zR)[R][C], float* zout,
+                                            long long zst, float* bs, long long bss) {
+    using RL = Rec<R, C>;
+    const int nint = nw - 1;
+    auto T = [&](int s) { return recs + (long long)s * cs; };
+    BWin<R, C, false> w;
+    w.clear_all();
+    for (int s = 0; s < nint; ++s) {
+        enter_block<R, C, false>(w, T(s), T(s + 1), (int)rs, true, s > 0, s > 0);
+        if (s == 0 && has_l) {  // known left separator: its coupling moves to the RHS
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm)
+#pragma unroll
+                for (int mp = 0; mp < R; ++mp) {
+                    const float x = T(0)[(RL::TCROSS + mm * R + mp) * rs];
+                    w.e[R + mm] += x;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) w.g[R + mm][c] = fmaf(x, zL[mp][c], w.g[R + mm][c]);
+                }
+        }
+        if (s == nint - 1 && has_r) {  // known right separator (its cross toward this block)
+            const float* tr = T(nw - 1);
+#pragma unroll
+            for (int ms = 0; ms < R; ++ms)
+#pragma unroll
+                for (int mm = 0; mm < R; ++mm) {
+                    const float x = tr[(RL::TCROSS + ms * R + mm) * rs];
+                    w.e[R + mm] += x;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) w.g[R + mm][c] = fmaf(x, zR[ms][c], w.g[R + mm][c]);
+                }
+        }
+        if (s > 0) {
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, false, bs + ((long long)((s - 1) * R + mm) * RL::RS) * bss, (int)bss);
+        }
+        w.shift();
+    }
+    if (nint > 0) {
+        w.clear_hi();
+#pragma unroll
+        for (int mm = 0; mm < R; ++mm) w.elim(0, mm, false, bs + ((long long)((nint - 1) * R + mm) * RL::RS) * bss, (int)bss);
+    }
+    float zn[R][C];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) zn[q][c] = 0.f;
+    for (int s = nint - 1; s >= 0; --s) {
+        float zc[R][C];
+#pragma unroll
+        for (int mm = R - 1; mm >= 0; --mm) {
+            const float* o = bs + ((long long)(s * R + mm) * RL::RS) * bss;
+#pragma unroll
+            for (int c = 0; c < C; ++c) zc[mm][c] = o[(2 * R - 1 + c) * bss];
+#pragma unroll
+            for (int i = mm + 1; i < 2 * R; ++i) {
+                const float ci = o[(i - mm - 1) * bss];
+#pragma unroll
+                for (int c = 0; c < C; ++c)
+                    zc[mm][c] = fmaf(ci, (i < R) ? zc[i < R ? i : 0][c] : zn[i >= R ? i - R : 0][c], zc[mm][c]);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                zout[((long long)(s * R + q) * C + c) * zst] = zc[q][c];
+                zn[q][c] = zc[q][c];
+            }
+    }
+}
+
+// ===================================================================== K2 (tree)
+//
+// Reduced system over the super-separators of one line, solved by a CTA of NG
+// warps x 32 lines: warp w reduces its group of consecutive super records to
+// one group record (level 1, in parallel), warp 0 solves the short group-level
+// system (level 2), then every warp solves its group's inner super-separators
+// with the two group separators as boundary values (level 3, in parallel).
+// Sequential depth ~ 2*PS/NG + NG instead of 2*PS.
+template <int R, int C>
+__global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __restrict__ rec,
+                                               float* __restrict__ rsc, float* __restrict__ z) {
+    using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, w = threadIdx.y, NG = blockDim.y;
+    const int NL = g.nb * g.batch;
+    const int L = blockIdx.x * 32 + lane;
+    const bool ok = L < NL;
+    const long long NLl = NL;
+    const int PSn = g.P;  // super records
+    const int NGa = min(NG, PSn);
+    const int J0 = (int)((long long)w * PSn / NGa), J1 = (int)((long long)(w + 1) * PSn / NGa);
+    const int gsz = J1 - J0;
+    const int rsG = NG * 32 + 1;
+    float* grec = sm;
+    float* zg = grec + RL::REC * rsG;
+    float* bsg = zg + NG * R * C * 32;
+    const float* my = rec + (long long)J0 * RL::REC * NLl + L;
+    if (w < NGa && ok)
+        reduce_super<R, C>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
+    __syncthreads();
+    float z0[R][C];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) z0[q][c] = 0.f;
+    if (w == 0 && ok && NGa > 1) solve_inner<R, C>(grec + lane, rsG, 32, NGa, false, z0, false, z0, zg + lane, 32, bsg + lane, 32);
+    __syncthreads();
+    if (w < NGa && ok) {
+        const bool has_l = w > 0, has_r = w < NGa - 1;
+        float zL[R][C], zR[R][C];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                zL[q][c] = has_l ? zg[(((w - 1) * R + q) * C + c) * 32 + lane] : 0.f;
+                zR[q][c] = has_r ? zg[((w * R + q) * C + c) * 32 + lane] : 0.f;
+            }
+        solve_inner<R, C>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
+                          z + (long long)J0 * R * C * NLl + L, NLl, rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
+        if (has_r) {
+            float* zo = z + (long long)(J1 - 1) * R * C * NLl + L;
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
+        }
+    }
+}
+
+template <int R, int C>
+__host__ inline size_t k2_tree_smem(int NG) {
+    using RL = Rec<R, C>;
+    return ((size_t)RL::REC * (NG * 32 + 1) + (size_t)NG * R * C * 32 + (size_t)NG * R * RL::RS * 32) * sizeof(float);
 }
 
 // ===================================================================== KA
@@ -576,12 +722,12 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
     float* bsc = zint + NW * R * C * 32;                 // (NW) x R x RS x 32 back-substitution rows
     const int stS = NT + 1;                              // state stride
     float* state = sm;                                   // K x NF x stS (overlays the above)
-    const int region1 = max(RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32, K * NF * stS);
+    const int region1 = (max(RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32, K * NF * stS) + 3) & ~3;
     float* tl = sm + region1;                            // output tile
     const int bl = min(B0 + 32, g.nb) - 1;
     const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
     const int ncol = xb - xa + 1;
-    const int TP = TR * C + 1;                           // tile pitch (per x line)
+    const int TP = ((TR * C + 3) & ~3) + 4;              // tile pitch (per x line), 16-byte rows
 
     // ---- 1. spike-forward of every chunk (records to smem)
     ChunkIn<R, C, CG, RW> in;
@@ -607,79 +753,7 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
                 zL[q][c] = has_l ? zs[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
                 zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
             }
-        const int nint = nw - 1;  // inner separators sigma_{J*NW + i}, i < nint
-        const float* r0 = recs + lane;
-        auto T = [&](int s) { return r0 + (long long)s * 32; };  // record of tile chunk s (field stride rs)
-        BWin<R, C, false> w;
-        w.clear_all();
-        float* bs0 = bsc + lane;  // back-substitution rows: [(i*R+mm)*RS + field]*32
-        for (int s = 0; s < nint; ++s) {
-            enter_block<R, C, false>(w, T(s), T(s + 1), rs, true, s > 0, s > 0);
-            if (s == 0 && has_l) {  // known left separator: move its coupling to the RHS
-#pragma unroll
-                for (int mm = 0; mm < R; ++mm)
-#pragma unroll
-                    for (int mp = 0; mp < R; ++mp) {
-                        const float x = T(0)[(RL::TCROSS + mm * R + mp) * rs];
-                        w.e[R + mm] += x;
-#pragma unroll
-                        for (int c = 0; c < C; ++c) w.g[R + mm][c] = fmaf(x, zL[mp][c], w.g[R + mm][c]);
-                    }
-            }
-            if (s == nint - 1 && has_r) {  // known right separator (its cross toward this block)
-                const float* tr = T(nw - 1);
-#pragma unroll
-                for (int ms = 0; ms < R; ++ms)
-#pragma unroll
-                    for (int mm = 0; mm < R; ++mm) {
-                        const float x = tr[(RL::TCROSS + ms * R + mm) * rs];
-                        w.e[R + mm] += x;
-#pragma unroll
-                        for (int c = 0; c < C; ++c) w.g[R + mm][c] = fmaf(x, zR[ms][c], w.g[R + mm][c]);
-                    }
-            }
-            if (s > 0) {
-#pragma unroll
-                for (int mm = 0; mm < R; ++mm)
-                    w.elim(0, mm, false, bs0 + ((long long)((s - 1) * R + mm) * RL::RS) * 32, 32);
-            }
-            w.shift();
-        }
-        if (nint > 0) {
-            w.clear_hi();
-#pragma unroll
-            for (int mm = 0; mm < R; ++mm)
-                w.elim(0, mm, false, bs0 + ((long long)((nint - 1) * R + mm) * RL::RS) * 32, 32);
-        }
-        float zn[R][C];
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-#pragma unroll
-            for (int c = 0; c < C; ++c) zn[q][c] = 0.f;
-        for (int s = nint - 1; s >= 0; --s) {
-            float zc[R][C];
-#pragma unroll
-            for (int mm = R - 1; mm >= 0; --mm) {
-                const float* o = bs0 + ((long long)(s * R + mm) * RL::RS) * 32;
-#pragma unroll
-                for (int c = 0; c < C; ++c) zc[mm][c] = o[(2 * R - 1 + c) * 32];
-#pragma unroll
-                for (int i = mm + 1; i < 2 * R; ++i) {
-                    const float ci = o[(i - mm - 1) * 32];
-#pragma unroll
-                    for (int c = 0; c < C; ++c)
-                        zc[mm][c] = fmaf(ci, (i < R) ? zc[i < R ? i : 0][c] : zn[i >= R ? i - R : 0][c], zc[mm][c]);
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < R; ++q)
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    zint[((s * R + q) * C + c) * 32 + lane] = zc[q][c];
-                    zn[q][c] = zc[q][c];
-                }
-        }
-        // the tile's boundary separators, for the chunks that touch them
+        solve_inner<R, C>(recs + lane, rs, 32, nw, has_l, zL, has_r, zR, zint + lane, 32, bsc + lane, 32);
         if (has_r) {
 #pragma unroll
             for (int q = 0; q < R; ++q)
@@ -806,7 +880,7 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         }
     }
     // ---- 4. averaging into the shared output tile, fixed phase order
-    for (int i = tid; i < ncol * TP; i += NT) tl[i] = 0.f;
+    for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     for (int ph = 0; ph < to.nph; ++ph) {
         if (active && (lane % to.nph) == ph) {
@@ -822,19 +896,44 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         }
         __syncthreads();
     }
-    // ---- 5. owned columns -> global, coalesced
+    // ---- 5. owned columns -> global, coalesced.  Column ownership / counts are
+    //         computed lane-parallel (32 columns per warp step) and broadcast.
     float* oi = to.out + img * g.img_stride;
     if (to.transpose_out) {
-        for (int xl = wid; xl < ncol; xl += NW) {
-            const int x = xa + xl;
-            int bmin, bmax;
-            covering(g, x, bmin, bmax);
-            const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
-            if (own != (int)blockIdx.x) continue;
-            const float inv_cnt = 1.0f / (float)(bmax - bmin + 1);
-            float* orow = oi + ((long long)x * g.Hl + Y0) * C;
-            const float* trow = tl + xl * TP;
-            for (int e2 = lane; e2 < TR * C; e2 += 32) orow[e2] = trow[e2] * inv_cnt;
+        const int n = TR * C;
+        for (int xb = wid * 32; xb < ncol; xb += NW * 32) {
+            float my_inv = 0.f;
+            {
+                const int x = xa + xb + lane;
+                if (xb + lane < ncol) {
+                    int bmin, bmax;
+                    covering(g, x, bmin, bmax);
+                    const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
+                    if (own == (int)blockIdx.x) my_inv = 1.0f / (float)(bmax - bmin + 1);
+                }
+            }
+            const int cnt = min(32, ncol - xb);
+            for (int i = 0; i < cnt; ++i) {
+                const float inv_cnt = __shfl_sync(0xffffffffu, my_inv, i);
+                if (inv_cnt == 0.f) continue;  // not owned by this CTA
+                const int xl = xb + i;
+                float* orow = oi + ((long long)(xa + xl) * g.Hl + Y0) * C;
+                const float* trow = tl + xl * TP;
+                if ((reinterpret_cast<uintptr_t>(orow) & 15) == 0) {
+                    const int n4 = n >> 2;
+                    for (int e4 = lane; e4 < n4; e4 += 32) {
+                        float4 v = reinterpret_cast<const float4*>(trow)[e4];
+                        v.x *= inv_cnt;
+                        v.y *= inv_cnt;
+                        v.z *= inv_cnt;
+                        v.w *= inv_cnt;
+                        reinterpret_cast<float4*>(orow)[e4] = v;
+                    }
+                    for (int e2 = (n4 << 2) + lane; e2 < n; e2 += 32) orow[e2] = trow[e2] * inv_cnt;
+                } else {
+                    for (int e2 = lane; e2 < n; e2 += 32) orow[e2] = trow[e2] * inv_cnt;
+                }
+            }
         }
     } else {
         for (int yl = wid; yl < TR; yl += NW) {
@@ -862,8 +961,8 @@ __host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
     const int NT = NW * 32;
     const size_t r1a = (size_t)RL::REC * (NT + 1) + (size_t)NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32;
     const size_t r1b = (size_t)K * NF * (NT + 1);
-    const size_t r1 = r1a > r1b ? r1a : r1b;
-    return (r1 + (size_t)ncol * (TR * C + 1)) * sizeof(float);
+    const size_t r1 = ((r1a > r1b ? r1a : r1b) + 3) & ~(size_t)3;
+    return (r1 + (size_t)ncol * (((TR * C + 3) & ~3) + 4)) * sizeof(float);
 }
 
 
@@ -889,7 +988,11 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             ProfScope ps("k2_reduced", st);
             PassGeom gs = g;
             gs.P = PS;
-            fast::k2_fast<R, C, 4><<<(NL + 31) / 32, 32, 0, st>>>(gs, pl.rec, pl.rs, pl.z);
+            const int NG = PS >= 64 ? 16 : 8;
+            const size_t sm2 = k2_tree_smem<R, C>(NG);
+            e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+            if (e != cudaSuccess) return e;
+            k2_tree<R, C><<<(NL + 31) / 32, dim3(32, NG), sm2, st>>>(gs, pl.rec, pl.rs, pl.z);
         }
     }
     {

@@ -168,6 +168,24 @@ def test_device_api_matches_host():
     assert np.array_equal(out.cpu().numpy(), host)
 
 
+def test_graph_replay_matches_direct():
+    import torch
+
+    rng = np.random.default_rng(16)
+    t = torch.from_numpy(_piecewise(rng, 130, 90, 3)).cuda()
+    g = torch.from_numpy(_piecewise(rng, 130, 90, 1)).cuda()
+    cfg = _cfg(400.0, 2, 3, 4, 1, 0)
+    direct = S.smooth_device(t, g, cfg, sync=True)
+    out = torch.empty_like(t)
+    for _ in range(3):  # capture, then replays
+        out.zero_()
+        S.smooth_device(t, g, cfg, out=out, graph=True, sync=True)
+        assert torch.equal(out, direct)
+    t.mul_(0.5)  # same buffers, new contents: the replay must see them
+    S.smooth_device(t, g, cfg, out=out, graph=True, sync=True)
+    assert torch.equal(out, S.smooth_device(t, g, cfg, sync=True))
+
+
 # ------------------------------------------------ BASELINE configurations
 
 def _full(name, port, max_images=None):
