@@ -11,7 +11,7 @@ import os
 from .config import Axis, CudaError, Error, SmoothConfig, WeightKind
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libsgwls_b200.so")
+LIB_PATH = os.environ.get("SGWLS_B200_LIB") or os.path.join(PKG, "libsgwls_b200.so")
 
 OK, EINVAL, ECUDA, EUNSUPPORTED = 0, 1, 2, 3
 SYNC, VALIDATE, GRAPH = 1, 2, 4

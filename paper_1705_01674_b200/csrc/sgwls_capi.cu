@@ -20,6 +20,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/sgwls_b200.h"
 #include "sgwls_kernels.h"
@@ -177,10 +178,19 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
     g.img_stride = (long long)Hl * Wl * C;
     g.gimg_stride = (long long)Hl * Wl * Cg;
     const long long NL = (long long)g.nb * batch;
-    ap.fast = (!g.degenerate && r <= kTileMaxR && (Cg == 1 || Cg == 3)) ? 1 : 0;
+    static const int force_generic = [] {
+        const char* v = std::getenv("SGWLS_FORCE_GENERIC");  // debugging knob: bypass the tiled path
+        return v ? std::atoi(v) : 0;
+    }();
+    static const int tile_warps = [] {
+        const char* v = std::getenv("SGWLS_TILE_WARPS");  // tuning knob: chunks per CTA tile
+        const int n = v ? std::atoi(v) : kTileWarps;
+        return n < 1 ? 1 : (n > 16 ? 16 : n);
+    }();
+    ap.fast = (!force_generic && !g.degenerate && r <= kTileMaxR && (Cg == 1 || Cg == 3)) ? 1 : 0;
     ap.step = 32;
     ap.ncta = 1;
-    ap.nw = kTileWarps;
+    ap.nw = tile_warps;
     ap.nph = 1;
     ap.bx = 128;
     if (ap.fast) {
@@ -356,6 +366,15 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.err = (p == 0) ? d_err : nullptr;
         pl.w = &wd;
         CK(launch_pass(pl, st));
+        if (p == 0 && std::getenv("SGWLS_DEBUG_Z") && z.p && z_n) {  // debugging aid: dump pass-0 separators
+            std::vector<float> hz(z_n);
+            CK(cudaMemcpyAsync(hz.data(), z.p, z_n * sizeof(float), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (FILE* f = std::fopen(std::getenv("SGWLS_DEBUG_Z"), "wb")) {
+                std::fwrite(hz.data(), sizeof(float), z_n, f);
+                std::fclose(f);
+            }
+        }
         src = out;
     }
 }

@@ -57,6 +57,10 @@ __host__ __device__ constexpr int rows_per_chunk(int R, int C) { return tile_row
 
 __device__ __forceinline__ constexpr int offi(int i, int j, int R) { return i * R - i * (i + 1) / 2 + (j - i - 1); }
 
+// clamp a (compile-time) register-array index into [0, n): indices in branches
+// that are dead for a given unrolled iteration must still be in bounds
+__host__ __device__ constexpr int cl(int x, int n) { return x < 0 ? 0 : (x >= n ? n - 1 : x); }
+
 // squared 2-D distance of the edge (q - t, q), q at in-row index jj (regular band)
 __host__ __device__ constexpr int edge_d2(int jj, int t) {
     return jj >= t ? t * t : 1 + (t - 1 - 2 * jj) * (t - 1 - 2 * jj);
@@ -125,7 +129,7 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
             float r2 = 0.f;
 #pragma unroll
             for (int c = 0; c < CG; ++c) {
-                const float other = (k - t >= 0) ? gp[k - t >= 0 ? k - t : 0][c] : gprev[(k - t + R) >= 0 ? (k - t + R) : 0][c];
+                const float other = (k - t >= 0) ? gp[cl(k - t, K)][c] : gprev[cl(k - t + R, R)][c];
                 const float d = gp[k][c] - other;
                 r2 = fmaf(d, d, r2);
             }
@@ -252,7 +256,7 @@ __device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>&
                 if (k - t >= 0) {
                     w.A[R - t][R] = lw;
                 } else if (has_left) {
-                    w.Q[R][(R - t + k) >= 0 ? (R - t + k) : 0] = lw;
+                    w.Q[R][cl(R - t + k, R)] = lw;
                 }
             }
             if (k >= R) {
@@ -613,15 +617,15 @@ __global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __
                 zL[q][c] = has_l ? zg[(((w - 1) * R + q) * C + c) * 32 + lane] : 0.f;
                 zR[q][c] = has_r ? zg[((w * R + q) * C + c) * 32 + lane] : 0.f;
             }
-        solve_inner<R, C>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
-                          z + (long long)J0 * R * C * NLl + L, NLl, rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
-        if (has_r) {
+        if (has_r) {  // stored before the solve (see kb_tile step 2)
             float* zo = z + (long long)(J1 - 1) * R * C * NLl + L;
 #pragma unroll
             for (int q = 0; q < R; ++q)
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
+        solve_inner<R, C>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
+                          z + (long long)J0 * R * C * NLl + L, NLl, rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
     }
 }
 
@@ -720,9 +724,7 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
     float* recs = sm;                                    // REC x rs
     float* zint = recs + RL::REC * rs;                   // NW x R*C x 32
     float* bsc = zint + NW * R * C * 32;                 // (NW) x R x RS x 32 back-substitution rows
-    const int stS = NT + 1;                              // state stride
-    float* state = sm;                                   // K x NF x stS (overlays the above)
-    const int region1 = (max(RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32, K * NF * stS) + 3) & ~3;
+    const int region1 = (RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32 + 3) & ~3;
     float* tl = sm + region1;                            // output tile
     const int bl = min(B0 + 32, g.nb) - 1;
     const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
@@ -753,7 +755,9 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
                 zL[q][c] = has_l ? zs[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
                 zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
             }
-        solve_inner<R, C>(recs + lane, rs, 32, nw, has_l, zL, has_r, zR, zint + lane, 32, bsc + lane, 32);
+        // The boundary values are stored BEFORE the solve: nvcc 12.9 was seen to
+        // reuse the register holding `nw` as the back-substitution loop counter
+        // and then address `zint[nw - 1]` with the decremented value.
         if (has_r) {
 #pragma unroll
             for (int q = 0; q < R; ++q)
@@ -765,6 +769,7 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         for (int q = 0; q < R; ++q)
 #pragma unroll
             for (int c = 0; c < C; ++c) bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane] = zL[q][c];
+        solve_inner<R, C>(recs + lane, rs, 32, nw, has_l, zL, has_r, zR, zint + lane, 32, bsc + lane, 32);
     }
     __syncthreads();
 
@@ -789,24 +794,43 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
                 if (!lastc) zr[q][c] = zint[((wid * R + q) * C + c) * 32 + lane];
             }
     }
-    __syncthreads();  // the state array overlays recs / zint / bsc
     const int kv = nrows * M;
     const int kend = lastc ? kv : kv - R;  // interior positions [0, kend)
+    // per-column output scale (1/count if this CTA owns the column, else 0)
+    float* inv_col = tl + ncol * TP;
+    for (int xl = tid; xl < ncol; xl += NT) {
+        int bmin, bmax;
+        covering(g, xa + xl, bmin, bmax);
+        const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
+        inv_col[xl] = own == (int)blockIdx.x ? 1.0f / (float)(bmax - bmin + 1) : 0.f;
+    }
+    for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+
+    // chunk factor state in registers: couplings cs[p][i] and y / u values ys[p][c]
+    float cs[K][R], ys[K][C];
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) cs[p][i] = 0.f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) ys[p][c] = 0.f;
+    }
     if (active) {
         Win<R, C, false> w;
         w.clear();
-        float* st = state + tid;
+        // positions k >= kv (short last chunk) enter as empty rows; the R extra
+        // steps drain the window
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            if (k < kv) {
+        for (int k = 0; k < K + R; ++k) {
+            if (k < K && k < kv) {
                 const bool kq = !lastc && (k >= K - R);  // known separator position (full chunk)
                 if (!kq) {
                     w.e[R] = 1.f;
 #pragma unroll
-                    for (int c = 0; c < C; ++c) w.g[R][c] = in.f[k][c];
+                    for (int c = 0; c < C; ++c) w.g[R][c] = in.f[cl(k, K)][c];
                 } else {
 #pragma unroll
-                    for (int c = 0; c < C; ++c) st[(k * NF + R + c) * stS] = zr[(k - (K - R)) >= 0 ? k - (K - R) : 0][c];
+                    for (int c = 0; c < C; ++c) ys[cl(k, K)][c] = zr[cl(k - (K - R), R)][c];
                 }
 #pragma unroll
                 for (int t = 1; t <= R; ++t) {
@@ -815,138 +839,106 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
                     const bool pleft = (k - t < 0);
                     const bool pright = kq && (k - t >= K - R);
                     if (pright) continue;
-                    const float lw = lam * in.w[k][t - 1];
+                    const float lw = lam * in.w[cl(k, K)][t - 1];
                     if (!kq && !pleft) {
                         w.A[R - t][R] = lw;
                     } else if (!kq && pleft) {
                         w.e[R] += lw;
 #pragma unroll
                         for (int c = 0; c < C; ++c)
-                            w.g[R][c] = fmaf(lw, zl[(R - t + k) >= 0 ? (R - t + k) : 0][c], w.g[R][c]);
+                            w.g[R][c] = fmaf(lw, zl[cl(R - t + k, R)][c], w.g[R][c]);
                     } else {
                         w.e[R - t] += lw;
 #pragma unroll
                         for (int c = 0; c < C; ++c)
-                            w.g[R - t][c] = fmaf(lw, zr[(k - (K - R)) >= 0 ? k - (K - R) : 0][c], w.g[R - t][c]);
+                            w.g[R - t][c] = fmaf(lw, zr[cl(k - (K - R), R)][c], w.g[R - t][c]);
                     }
                 }
-                if (k >= R) {
-                    float cc[R + 1];
-                    const float inv = w.elim(cc, false);
-#pragma unroll
-                    for (int i = 1; i <= R; ++i) st[((k - R) * NF + i - 1) * stS] = cc[i];
-#pragma unroll
-                    for (int c = 0; c < C; ++c) st[((k - R) * NF + R + c) * stS] = w.g[0][c] * inv;
-                }
-                w.shift();
             }
-        }
-        if (lastc) {
-            for (int d = 0; d < R; ++d) {
+            const int pp = k - R;  // position eliminated at this step
+            if (pp >= 0 && pp < kend) {
                 float cc[R + 1];
                 const float inv = w.elim(cc, false);
-                const int kk = kv - R + d;
 #pragma unroll
-                for (int i = 1; i <= R; ++i) st[(kk * NF + i - 1) * stS] = cc[i];
+                for (int i = 1; i <= R; ++i) cs[cl(pp, K)][i - 1] = cc[i];
 #pragma unroll
-                for (int c = 0; c < C; ++c) st[(kk * NF + R + c) * stS] = w.g[0][c] * inv;
-                w.shift();
+                for (int c = 0; c < C; ++c) ys[cl(pp, K)][c] = w.g[0][c] * inv;
             }
+            w.shift();
         }
-        float ur[R][C];
+        // back substitution (u replaces y in place)
 #pragma unroll
-        for (int i = 0; i < R; ++i)
+        for (int p = K - 1; p >= 0; --p) {
+            if (p < kend) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) ur[i][c] = 0.f;
-        for (int k = kend - 1; k >= 0; --k) {
-            float u[C];
+                for (int i = 1; i <= R; ++i) {
+                    if (p + i < K) {
 #pragma unroll
-            for (int c = 0; c < C; ++c) u[c] = st[(k * NF + R + c) * stS];
-#pragma unroll
-            for (int i = 1; i <= R; ++i) {
-                const float ci = st[(k * NF + i - 1) * stS];
-#pragma unroll
-                for (int c = 0; c < C; ++c) u[c] = fmaf(ci, ur[i - 1][c], u[c]);
-            }
-#pragma unroll
-            for (int i = R - 1; i > 0; --i)
-#pragma unroll
-                for (int c = 0; c < C; ++c) ur[i][c] = ur[i - 1][c];
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                ur[0][c] = u[c];
-                st[(k * NF + R + c) * stS] = u[c];
+                        for (int c = 0; c < C; ++c) ys[p][c] = fmaf(cs[p][i - 1], ys[cl(p + i, K)][c], ys[p][c]);
+                    }
+                }
             }
         }
     }
-    // ---- 4. averaging into the shared output tile, fixed phase order
-    for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
+    // ---- 4. averaging into the shared output tile, fixed phase order
+    const int par0 = y0 & 1;
+    float* tbase = tl + (lo - xa) * TP + (y0 - Y0) * C;
     for (int ph = 0; ph < to.nph; ++ph) {
         if (active && (lane % to.nph) == ph) {
-            const float* st = state + tid;
-            for (int k = 0; k < kv; ++k) {
-                const int rr = k / M, jj = k - rr * M;
-                const int y = y0 + rr;
-                const int co = (y & 1) ? (M - 1 - jj) : jj;
-                float* tp = tl + (lo + co - xa) * TP + (y - Y0) * C;
 #pragma unroll
-                for (int c = 0; c < C; ++c) tp[c] += st[(k * NF + R + c) * stS];
+            for (int p = 0; p < K; ++p) {
+                if (p < kv) {
+                    constexpr int dummy = 0;
+                    (void)dummy;
+                    const int rr = p / M, jj = p % M;
+                    const int oe = jj * TP + rr * C, oo = (M - 1 - jj) * TP + rr * C;
+                    float* tp = tbase + (((par0 ^ (rr & 1)) != 0) ? oo : oe);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) tp[c] += ys[p][c];
+                }
             }
         }
         __syncthreads();
     }
-    // ---- 5. owned columns -> global, coalesced.  Column ownership / counts are
-    //         computed lane-parallel (32 columns per warp step) and broadcast.
+    // ---- 5. owned columns -> global, coalesced (flattened over the tile)
     float* oi = to.out + img * g.img_stride;
     if (to.transpose_out) {
         const int n = TR * C;
-        for (int xb = wid * 32; xb < ncol; xb += NW * 32) {
-            float my_inv = 0.f;
-            {
-                const int x = xa + xb + lane;
-                if (xb + lane < ncol) {
-                    int bmin, bmax;
-                    covering(g, x, bmin, bmax);
-                    const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
-                    if (own == (int)blockIdx.x) my_inv = 1.0f / (float)(bmax - bmin + 1);
-                }
+        const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
+                         ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
+        if (vec) {
+            const int n4 = n >> 2;
+            const int tot = ncol * n4;
+            for (int i = tid; i < tot; i += NT) {
+                const int xl = i / n4, e4 = i - xl * n4;
+                const float sc = inv_col[xl];
+                if (sc == 0.f) continue;
+                float4 v = reinterpret_cast<const float4*>(tl + xl * TP)[e4];
+                v.x *= sc;
+                v.y *= sc;
+                v.z *= sc;
+                v.w *= sc;
+                reinterpret_cast<float4*>(oi + ((long long)(xa + xl) * g.Hl + Y0) * C)[e4] = v;
             }
-            const int cnt = min(32, ncol - xb);
-            for (int i = 0; i < cnt; ++i) {
-                const float inv_cnt = __shfl_sync(0xffffffffu, my_inv, i);
-                if (inv_cnt == 0.f) continue;  // not owned by this CTA
-                const int xl = xb + i;
-                float* orow = oi + ((long long)(xa + xl) * g.Hl + Y0) * C;
-                const float* trow = tl + xl * TP;
-                if ((reinterpret_cast<uintptr_t>(orow) & 15) == 0) {
-                    const int n4 = n >> 2;
-                    for (int e4 = lane; e4 < n4; e4 += 32) {
-                        float4 v = reinterpret_cast<const float4*>(trow)[e4];
-                        v.x *= inv_cnt;
-                        v.y *= inv_cnt;
-                        v.z *= inv_cnt;
-                        v.w *= inv_cnt;
-                        reinterpret_cast<float4*>(orow)[e4] = v;
-                    }
-                    for (int e2 = (n4 << 2) + lane; e2 < n; e2 += 32) orow[e2] = trow[e2] * inv_cnt;
-                } else {
-                    for (int e2 = lane; e2 < n; e2 += 32) orow[e2] = trow[e2] * inv_cnt;
-                }
+        } else {
+            const int tot = ncol * n;
+            for (int i = tid; i < tot; i += NT) {
+                const int xl = i / n, e2 = i - xl * n;
+                const float sc = inv_col[xl];
+                if (sc == 0.f) continue;
+                oi[((long long)(xa + xl) * g.Hl + Y0) * C + e2] = tl[xl * TP + e2] * sc;
             }
         }
     } else {
-        for (int yl = wid; yl < TR; yl += NW) {
-            float* orow = oi + ((long long)(Y0 + yl) * g.Wl + xa) * C;
-            for (int e2 = lane; e2 < ncol * C; e2 += 32) {
-                const int xl = e2 / C, c = e2 - xl * C;
-                const int x = xa + xl;
-                int bmin, bmax;
-                covering(g, x, bmin, bmax);
-                const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
-                if (own != (int)blockIdx.x) continue;
-                orow[e2] = tl[xl * TP + yl * C + c] / (float)(bmax - bmin + 1);
-            }
+        const int rowlen = ncol * C;
+        const int tot = TR * rowlen;
+        for (int i = tid; i < tot; i += NT) {
+            const int yl = i / rowlen, e2 = i - yl * rowlen;
+            const int xl = e2 / C, c = e2 - xl * C;
+            const float sc = inv_col[xl];
+            if (sc == 0.f) continue;
+            oi[((long long)(Y0 + yl) * g.Wl + xa) * C + e2] = tl[xl * TP + yl * C + c] * sc;
         }
     }
 }
@@ -960,9 +952,10 @@ __host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
     using RL = Rec<R, C>;
     const int NT = NW * 32;
     const size_t r1a = (size_t)RL::REC * (NT + 1) + (size_t)NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32;
-    const size_t r1b = (size_t)K * NF * (NT + 1);
-    const size_t r1 = ((r1a > r1b ? r1a : r1b) + 3) & ~(size_t)3;
-    return (r1 + (size_t)ncol * (((TR * C + 3) & ~3) + 4)) * sizeof(float);
+    const size_t r1 = (r1a + 3) & ~(size_t)3;
+    (void)K;
+    (void)NF;
+    return (r1 + (size_t)ncol * (((TR * C + 3) & ~3) + 4) + ncol) * sizeof(float);
 }
 
 

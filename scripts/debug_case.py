@@ -21,8 +21,10 @@ def run(h, w, c, r, tau, T, kind, axis, lam=400.0, seed=0):
         ys, xs = np.nonzero(bad.any(axis=2))
         print("   bad rows", sorted(set(ys.tolist()))[:20], "cols", sorted(set(xs.tolist()))[:40])
 
-for args in [(40, 31, 3, 2, 2, 1, 0, 0), (40, 31, 3, 2, 2, 1, 0, 1), (40, 31, 1, 2, 2, 1, 1, 0), (64, 40, 1, 1, 1, 1, 1, 0),
+CASES = [(40, 31, 3, 2, 2, 1, 0, 0), (40, 31, 3, 2, 2, 1, 0, 1), (40, 31, 1, 2, 2, 1, 1, 0), (64, 40, 1, 1, 1, 1, 1, 0),
              (64, 40, 1, 1, 3, 1, 1, 0), (64, 40, 3, 1, 3, 1, 1, 0), (64, 40, 1, 2, 5, 1, 1, 0), (64, 40, 1, 2, 3, 1, 1, 0),
              (200, 40, 1, 2, 5, 1, 1, 0), (200, 40, 1, 1, 3, 1, 1, 0), (200, 100, 1, 1, 1, 1, 1, 0),
-             (200, 40, 1, 3, 7, 1, 1, 0), (512, 40, 1, 1, 3, 1, 1, 0)]:
-    run(*args)
+             (200, 40, 1, 3, 7, 1, 1, 0), (512, 40, 1, 1, 3, 1, 1, 0)]
+if __name__ == "__main__":
+    for args in CASES:
+        run(*args)
