@@ -102,17 +102,17 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
         const int y = y0 + rr;
         const bool valid = rr < nrows;
         const bool odd = y & 1;
+        const float* rowF = F + ((long long)y * g.Wl + lo) * C;
+        const float* rowG = G + ((long long)y * g.Wl + lo) * CG;
 #pragma unroll
         for (int jj = 0; jj < M; ++jj) {
             const int k = rr * M + jj;
             const int co = odd ? (M - 1 - jj) : jj;
             if (valid) {
-                const float* pf = F + ((long long)y * g.Wl + lo + co) * C;
-                const float* pg = G + ((long long)y * g.Wl + lo + co) * CG;
 #pragma unroll
-                for (int c = 0; c < C; ++c) in.f[k][c] = __ldg(pf + c);
+                for (int c = 0; c < C; ++c) in.f[k][c] = __ldg(rowF + co * C + c);
 #pragma unroll
-                for (int c = 0; c < CG; ++c) gp[k][c] = __ldg(pg + c);
+                for (int c = 0; c < CG; ++c) gp[k][c] = __ldg(rowG + co * CG + c);
             } else {
 #pragma unroll
                 for (int c = 0; c < C; ++c) in.f[k][c] = 0.f;
@@ -121,7 +121,10 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
             }
         }
     }
-    // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time
+    // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time.
+    // A NaN weight (NaN guidance) is the reference's "non-positive pivot" failure:
+    // remember the first offending position and report it once.
+    int bad = 0x7fffffff;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
 #pragma unroll
@@ -135,14 +138,12 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
             }
             const float wv = guidance_weight(W, r2, edge_d2(k % M, t));
             in.w[k][t - 1] = wv;
-            if (err != nullptr && !(wv >= 0.f)) {
-                // report only real edges: both ends exist
-                const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
-                if (exists)
-                    atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)(y0 * M + k - t));
-            }
+            const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
+            bad = (!(wv >= 0.f) && exists) ? min(bad, y0 * M + k - t) : bad;
         }
     }
+    if (err != nullptr && bad != 0x7fffffff)
+        atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)bad);
 }
 
 // ------------------------------------------------- elimination window (scalar)
@@ -237,16 +238,19 @@ struct Win {
 // Spike-forward over one chunk: eliminates the interior, leaves sigma_j in
 // slots 0..R-1 (non-last chunk) and the head update of sigma_{j-1}; writes the
 // chunk record into `rec` (stride `rs` floats between fields).
-template <int R, int C, int CG, int RW>
-__device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                    bool last, int kv, float* rec, int rs) {
+// FULL: the chunk has all RW rows (every chunk but possibly the band's last):
+// the position loop is then free of runtime predicates, so the window shifts
+// compile to register renames.
+template <int R, int C, int CG, int RW, bool FULL>
+__device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
+                                                         bool last, int kv, float* rec, int rs) {
     using RL = Rec<R, C>;
     constexpr int K = RW * (2 * R + 1);
     Win<R, C, true> w;
     w.clear();
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-        if (k < kv) {
+        if (FULL || k < kv) {
             w.e[R] = 1.f;
 #pragma unroll
             for (int c = 0; c < C; ++c) w.g[R][c] = in.f[k][c];
@@ -293,6 +297,15 @@ __device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>&
 #pragma unroll
         for (int c = 0; c < C; ++c) rec[(RL::HG + mm * C + c) * rs] = w.hg[mm][c];
     }
+}
+
+template <int R, int C, int CG, int RW>
+__device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
+                                                    bool last, int kv, float* rec, int rs) {
+    if (kv == RW * (2 * R + 1))
+        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs);
+    else
+        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lam, has_left, last, kv, rec, rs);
 }
 
 // ---------------------------------------------- block window (separator level)
@@ -671,6 +684,87 @@ __global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __
     }
 }
 
+// Interior solve of one chunk with both separators known (zl: previous
+// chunk's separator, zr: this chunk's): forward elimination with the known
+// couplings moved to the right-hand side, back substitution in registers.
+// FULL_INNER: full chunk that is not the band's last (kv = K, kend = K - R at
+// compile time); otherwise the general predicated form.
+template <int R, int C, int CG, int RW, bool FULL_INNER>
+__device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>& in, float lam, int j, bool lastc,
+                                                     int kv, int kend, const float (&zl)[R][C],
+                                                     const float (&zr)[R][C], float (&cs)[RW * (2 * R + 1)][R],
+                                                     float (&ys)[RW * (2 * R + 1)][C]) {
+    constexpr int M = 2 * R + 1, K = RW * M;
+    if (FULL_INNER) {
+        kv = K;
+        kend = K - R;
+        lastc = false;
+    }
+    Win<R, C, false> w;
+    w.clear();
+    // positions k >= kv (short last chunk) enter as empty rows; the R extra
+    // steps drain the window
+#pragma unroll
+    for (int k = 0; k < K + R; ++k) {
+        if (k < K && k < kv) {
+            const bool kq = !lastc && (k >= K - R);  // known separator position (full chunk)
+            if (!kq) {
+                w.e[R] = 1.f;
+#pragma unroll
+                for (int c = 0; c < C; ++c) w.g[R][c] = in.f[cl(k, K)][c];
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) ys[cl(k, K)][c] = zr[cl(k - (K - R), R)][c];
+            }
+#pragma unroll
+            for (int t = 1; t <= R; ++t) {
+                const bool pe = (k - t >= 0) || (j > 0);
+                if (!pe) continue;
+                const bool pleft = (k - t < 0);
+                const bool pright = kq && (k - t >= K - R);
+                if (pright) continue;
+                const float lw = lam * in.w[cl(k, K)][t - 1];
+                if (!kq && !pleft) {
+                    w.A[R - t][R] = lw;
+                } else if (!kq && pleft) {
+                    w.e[R] += lw;
+#pragma unroll
+                    for (int c = 0; c < C; ++c)
+                        w.g[R][c] = fmaf(lw, zl[cl(R - t + k, R)][c], w.g[R][c]);
+                } else {
+                    w.e[R - t] += lw;
+#pragma unroll
+                    for (int c = 0; c < C; ++c)
+                        w.g[R - t][c] = fmaf(lw, zr[cl(k - (K - R), R)][c], w.g[R - t][c]);
+                }
+            }
+        }
+        const int pp = k - R;  // position eliminated at this step
+        if (pp >= 0 && pp < kend) {
+            float cc[R + 1];
+            const float inv = w.elim(cc, false);
+#pragma unroll
+            for (int i = 1; i <= R; ++i) cs[cl(pp, K)][i - 1] = cc[i];
+#pragma unroll
+            for (int c = 0; c < C; ++c) ys[cl(pp, K)][c] = w.g[0][c] * inv;
+        }
+        w.shift();
+    }
+    // back substitution (u replaces y in place)
+#pragma unroll
+    for (int p = K - 1; p >= 0; --p) {
+        if (p < kend) {
+#pragma unroll
+            for (int i = 1; i <= R; ++i) {
+                if (p + i < K) {
+#pragma unroll
+                    for (int c = 0; c < C; ++c) ys[p][c] = fmaf(cs[p][i - 1], ys[cl(p + i, K)][c], ys[p][c]);
+                }
+            }
+        }
+    }
+}
+
 // ===================================================================== KB
 
 struct TileOut {
@@ -804,7 +898,8 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
         inv_col[xl] = own == (int)blockIdx.x ? 1.0f / (float)(bmax - bmin + 1) : 0.f;
     }
-    for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (to.nph > 1)
+        for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
 
     // chunk factor state in registers: couplings cs[p][i] and y / u values ys[p][c]
     float cs[K][R], ys[K][C];
@@ -816,72 +911,14 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         for (int c = 0; c < C; ++c) ys[p][c] = 0.f;
     }
     if (active) {
-        Win<R, C, false> w;
-        w.clear();
-        // positions k >= kv (short last chunk) enter as empty rows; the R extra
-        // steps drain the window
-#pragma unroll
-        for (int k = 0; k < K + R; ++k) {
-            if (k < K && k < kv) {
-                const bool kq = !lastc && (k >= K - R);  // known separator position (full chunk)
-                if (!kq) {
-                    w.e[R] = 1.f;
-#pragma unroll
-                    for (int c = 0; c < C; ++c) w.g[R][c] = in.f[cl(k, K)][c];
-                } else {
-#pragma unroll
-                    for (int c = 0; c < C; ++c) ys[cl(k, K)][c] = zr[cl(k - (K - R), R)][c];
-                }
-#pragma unroll
-                for (int t = 1; t <= R; ++t) {
-                    const bool pe = (k - t >= 0) || (j > 0);
-                    if (!pe) continue;
-                    const bool pleft = (k - t < 0);
-                    const bool pright = kq && (k - t >= K - R);
-                    if (pright) continue;
-                    const float lw = lam * in.w[cl(k, K)][t - 1];
-                    if (!kq && !pleft) {
-                        w.A[R - t][R] = lw;
-                    } else if (!kq && pleft) {
-                        w.e[R] += lw;
-#pragma unroll
-                        for (int c = 0; c < C; ++c)
-                            w.g[R][c] = fmaf(lw, zl[cl(R - t + k, R)][c], w.g[R][c]);
-                    } else {
-                        w.e[R - t] += lw;
-#pragma unroll
-                        for (int c = 0; c < C; ++c)
-                            w.g[R - t][c] = fmaf(lw, zr[cl(k - (K - R), R)][c], w.g[R - t][c]);
-                    }
-                }
-            }
-            const int pp = k - R;  // position eliminated at this step
-            if (pp >= 0 && pp < kend) {
-                float cc[R + 1];
-                const float inv = w.elim(cc, false);
-#pragma unroll
-                for (int i = 1; i <= R; ++i) cs[cl(pp, K)][i - 1] = cc[i];
-#pragma unroll
-                for (int c = 0; c < C; ++c) ys[cl(pp, K)][c] = w.g[0][c] * inv;
-            }
-            w.shift();
-        }
-        // back substitution (u replaces y in place)
-#pragma unroll
-        for (int p = K - 1; p >= 0; --p) {
-            if (p < kend) {
-#pragma unroll
-                for (int i = 1; i <= R; ++i) {
-                    if (p + i < K) {
-#pragma unroll
-                        for (int c = 0; c < C; ++c) ys[p][c] = fmaf(cs[p][i - 1], ys[cl(p + i, K)][c], ys[p][c]);
-                    }
-                }
-            }
-        }
+        if (!lastc && kv == K)
+            chunk_interior_solve<R, C, CG, RW, true>(in, lam, j, lastc, kv, kend, zl, zr, cs, ys);
+        else
+            chunk_interior_solve<R, C, CG, RW, false>(in, lam, j, lastc, kv, kend, zl, zr, cs, ys);
     }
     __syncthreads();
     // ---- 4. averaging into the shared output tile, fixed phase order
+    //         (nph == 1: no two bands overlap, every tile cell has one writer)
     const int par0 = y0 & 1;
     float* tbase = tl + (lo - xa) * TP + (y0 - Y0) * C;
     for (int ph = 0; ph < to.nph; ++ph) {
@@ -889,56 +926,62 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
 #pragma unroll
             for (int p = 0; p < K; ++p) {
                 if (p < kv) {
-                    constexpr int dummy = 0;
-                    (void)dummy;
                     const int rr = p / M, jj = p % M;
                     const int oe = jj * TP + rr * C, oo = (M - 1 - jj) * TP + rr * C;
                     float* tp = tbase + (((par0 ^ (rr & 1)) != 0) ? oo : oe);
+                    if (to.nph == 1) {
 #pragma unroll
-                    for (int c = 0; c < C; ++c) tp[c] += ys[p][c];
+                        for (int c = 0; c < C; ++c) tp[c] = ys[p][c];
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < C; ++c) tp[c] += ys[p][c];
+                    }
                 }
             }
         }
         __syncthreads();
     }
-    // ---- 5. owned columns -> global, coalesced (flattened over the tile)
+    // ---- 5. owned columns -> global, coalesced.  A warp writes `per` whole
+    //         output columns (transposed layout: TR*C contiguous floats each)
+    //         per step, lanes split as (column, float4) -- no per-element division.
     float* oi = to.out + img * g.img_stride;
     if (to.transpose_out) {
         const int n = TR * C;
         const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
-        if (vec) {
-            const int n4 = n >> 2;
-            const int tot = ncol * n4;
-            for (int i = tid; i < tot; i += NT) {
-                const int xl = i / n4, e4 = i - xl * n4;
-                const float sc = inv_col[xl];
-                if (sc == 0.f) continue;
-                float4 v = reinterpret_cast<const float4*>(tl + xl * TP)[e4];
-                v.x *= sc;
-                v.y *= sc;
-                v.z *= sc;
-                v.w *= sc;
-                reinterpret_cast<float4*>(oi + ((long long)(xa + xl) * g.Hl + Y0) * C)[e4] = v;
-            }
-        } else {
-            const int tot = ncol * n;
-            for (int i = tid; i < tot; i += NT) {
-                const int xl = i / n, e2 = i - xl * n;
-                const float sc = inv_col[xl];
-                if (sc == 0.f) continue;
-                oi[((long long)(xa + xl) * g.Hl + Y0) * C + e2] = tl[xl * TP + e2] * sc;
+        const int nv = vec ? (n >> 2) : n;      // vectors per column
+        const int per = nv >= 32 ? 1 : 32 / nv;  // columns per warp step
+        const int sub = nv >= 32 ? 0 : lane / nv;
+        const int e0 = nv >= 32 ? lane : lane - sub * nv;
+        const int estep = nv >= 32 ? 32 : nv;
+        for (int xb = wid * per; xb < ncol; xb += NW * per) {
+            const int xl = xb + sub;
+            if (sub >= per || xl >= ncol) continue;
+            const float sc = inv_col[xl];
+            if (sc == 0.f) continue;
+            const float* trow = tl + xl * TP;
+            float* orow = oi + ((long long)(xa + xl) * g.Hl + Y0) * C;
+            if (vec) {
+                for (int e4 = e0; e4 < nv; e4 += estep) {
+                    float4 v = reinterpret_cast<const float4*>(trow)[e4];
+                    v.x *= sc;
+                    v.y *= sc;
+                    v.z *= sc;
+                    v.w *= sc;
+                    reinterpret_cast<float4*>(orow)[e4] = v;
+                }
+            } else {
+                for (int e2 = e0; e2 < nv; e2 += estep) orow[e2] = trow[e2] * sc;
             }
         }
     } else {
-        const int rowlen = ncol * C;
-        const int tot = TR * rowlen;
-        for (int i = tid; i < tot; i += NT) {
-            const int yl = i / rowlen, e2 = i - yl * rowlen;
-            const int xl = e2 / C, c = e2 - xl * C;
-            const float sc = inv_col[xl];
-            if (sc == 0.f) continue;
-            oi[((long long)(Y0 + yl) * g.Wl + xa) * C + e2] = tl[xl * TP + yl * C + c] * sc;
+        for (int yl = wid; yl < TR; yl += NW) {
+            float* orow = oi + ((long long)(Y0 + yl) * g.Wl + xa) * C;
+            for (int e2 = lane; e2 < ncol * C; e2 += 32) {
+                const int xl = e2 / C, c = e2 - xl * C;
+                const float sc = inv_col[xl];
+                if (sc != 0.f) orow[e2] = tl[xl * TP + yl * C + c] * sc;
+            }
         }
     }
 }
