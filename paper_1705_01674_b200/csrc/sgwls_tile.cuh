@@ -953,7 +953,6 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         const int per = nv >= 32 ? 1 : 32 / nv;  // columns per warp step
         const int sub = nv >= 32 ? 0 : lane / nv;
         const int e0 = nv >= 32 ? lane : lane - sub * nv;
-        const int estep = nv >= 32 ? 32 : nv;
         for (int xb = wid * per; xb < ncol; xb += NW * per) {
             const int xl = xb + sub;
             if (sub >= per || xl >= ncol) continue;
@@ -961,17 +960,28 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
             if (sc == 0.f) continue;
             const float* trow = tl + xl * TP;
             float* orow = oi + ((long long)(xa + xl) * g.Hl + Y0) * C;
+            // constant-stride loops only: a runtime stride costs an integer
+            // division per column for the trip count
             if (vec) {
-                for (int e4 = e0; e4 < nv; e4 += estep) {
+                auto put4 = [&](int e4) {
                     float4 v = reinterpret_cast<const float4*>(trow)[e4];
                     v.x *= sc;
                     v.y *= sc;
                     v.z *= sc;
                     v.w *= sc;
                     reinterpret_cast<float4*>(orow)[e4] = v;
+                };
+                if (nv <= 32) {
+                    if (e0 < nv) put4(e0);
+                } else {
+                    for (int e4 = lane; e4 < nv; e4 += 32) put4(e4);
                 }
             } else {
-                for (int e2 = e0; e2 < nv; e2 += estep) orow[e2] = trow[e2] * sc;
+                if (nv <= 32) {
+                    if (e0 < nv) orow[e0] = trow[e0] * sc;
+                } else {
+                    for (int e2 = lane; e2 < nv; e2 += 32) orow[e2] = trow[e2] * sc;
+                }
             }
         }
     } else {
