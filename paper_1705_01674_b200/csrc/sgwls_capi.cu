@@ -182,11 +182,13 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         const char* v = std::getenv("SGWLS_FORCE_GENERIC");  // debugging knob: bypass the tiled path
         return v ? std::atoi(v) : 0;
     }();
-    static const int tile_warps = [] {
+    static const int tile_warps_env = [] {
         const char* v = std::getenv("SGWLS_TILE_WARPS");  // tuning knob: chunks per CTA tile
-        const int n = v ? std::atoi(v) : kTileWarps;
-        return n < 1 ? 1 : (n > 16 ? 16 : n);
+        const int n = v ? std::atoi(v) : 0;
+        return n < 0 ? 0 : (n > 8 ? 8 : n);
     }();
+    // measured on B200: 8-chunk tiles for r = 1, 4-chunk tiles for r >= 2
+    const int tile_warps = tile_warps_env ? tile_warps_env : (r == 1 ? kTileWarps : kTileWarps / 2);
     ap.fast = (!force_generic && !g.degenerate && r <= kTileMaxR && (Cg == 1 || Cg == 3)) ? 1 : 0;
     ap.step = 32;
     ap.ncta = 1;
@@ -252,7 +254,10 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
 }
 
 int kernels_per_pass(const AxisPlan& ap) {
-    if (ap.fast) return ((ap.g.P + ap.nw - 1) / ap.nw > 1 ? 2 : 0) + 1;
+    if (ap.fast) {  // ka_tile (K2 fused or its own k2_tree), kb_tile
+        const int PS = (ap.g.P + ap.nw - 1) / ap.nw;
+        return (PS > 1 ? (tile_fuse_k2(PS) ? 1 : 2) : 0) + 1;
+    }
     return (ap.g.P > 1 ? 2 : 0) + 2;
 }
 
@@ -316,7 +321,10 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         u_n = mx(u_n, ap1.u_n);
     }
     const size_t img_n = (size_t)batch * W * H * C;
-    DevBuf rec, rs, z, U, bufA, bufB, gt;
+    const size_t ngroups = (size_t)(mx(ap0.g.nb, ap1.g.nb) * batch + 31) / 32;
+    DevBuf rec, rs, z, U, bufA, bufB, gt, cnt;
+    cnt.alloc(ngroups, st);
+    CK(cudaMemsetAsync(cnt.p, 0, ngroups * sizeof(float), st));
     rec.alloc(rec_n, st);
     rs.alloc(rs_n, st);
     z.alloc(z_n, st);
@@ -347,6 +355,7 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.ncta = ap.ncta;
         pl.nw = ap.nw;
         pl.nph = ap.nph;
+        pl.counters = reinterpret_cast<int*>(cnt.p);
         pl.src = src;
         pl.guid = o == 0 ? d_g : gt.p;
         const bool lastp = (p == T - 1);

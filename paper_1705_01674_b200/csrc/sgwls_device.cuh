@@ -74,6 +74,11 @@ __host__ __device__ constexpr int tile_rows_per_chunk(int R, int C) {
 }
 constexpr int kTileMaxR = 4;
 constexpr int kTileWarps = 8;
+// K2 runs inside the last KA tile of each band group when the reduced system
+// is this short (sequential depth ~2*PS/NW + NW); longer systems get their own
+// 16-warp tree launch.
+constexpr int kFuseK2MaxSuper = 32;
+__host__ __device__ constexpr bool tile_fuse_k2(int PS) { return PS > 1 && PS <= kFuseK2MaxSuper; }
 
 __device__ __forceinline__ float fast_ex2(float x) {
     float y;

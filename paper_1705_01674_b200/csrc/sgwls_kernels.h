@@ -26,6 +26,7 @@ struct PassLaunch {
     float* U;           // band solutions
     unsigned long long* err;  // NaN-weight report (first pass only), or nullptr
     const WeightDev* w;
+    int* counters = nullptr;  // tiled path: per-band-group tile counters (zeroed; self-resetting)
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);

@@ -591,14 +591,15 @@ __device__ __forceinline__ void solve_inner(const float* recs, long long rs, lon
 // system (level 2), then every warp solves its group's inner super-separators
 // with the two group separators as boundary values (level 3, in parallel).
 // Sequential depth ~ 2*PS/NG + NG instead of 2*PS.
+// Body of the tree solve for one group of 32 lines (lane = line, w = warp),
+// usable both as its own kernel and from the last KA tile of a band group.
 template <int R, int C>
-__global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __restrict__ rec,
-                                               float* __restrict__ rsc, float* __restrict__ z) {
+__device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* __restrict__ rec,
+                                             float* __restrict__ rsc, float* __restrict__ z, float* sm, int lane,
+                                             int w, int NG, int group) {
     using RL = Rec<R, C>;
-    extern __shared__ float sm[];
-    const int lane = threadIdx.x, w = threadIdx.y, NG = blockDim.y;
     const int NL = g.nb * g.batch;
-    const int L = blockIdx.x * 32 + lane;
+    const int L = group * 32 + lane;
     const bool ok = L < NL;
     const long long NLl = NL;
     const int PSn = g.P;  // super records
@@ -643,6 +644,13 @@ __global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __
 }
 
 template <int R, int C>
+__global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __restrict__ rec,
+                                               float* __restrict__ rsc, float* __restrict__ z) {
+    extern __shared__ float sm[];
+    k2_tree_body<R, C>(g, rec, rsc, z, sm, threadIdx.x, threadIdx.y, blockDim.y, blockIdx.x);
+}
+
+template <int R, int C>
 __host__ inline size_t k2_tree_smem(int NG) {
     using RL = Rec<R, C>;
     return ((size_t)RL::REC * (NG * 32 + 1) + (size_t)NG * R * C * 32 + (size_t)NG * R * RL::RS * 32) * sizeof(float);
@@ -653,7 +661,8 @@ __host__ inline size_t k2_tree_smem(int NG) {
 template <int R, int C, int CG>
 __global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
-                                               const __grid_constant__ WeightDev W) {
+                                               float* __restrict__ rsc, float* __restrict__ zs,
+                                               int* __restrict__ counters, const __grid_constant__ WeightDev W) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1;
     using RL = Rec<R, C>;
@@ -677,11 +686,29 @@ __global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __
         chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0, j == g.P - 1, nrows * M, rec, rs);
     }
     __syncthreads();
+    const int PS = (g.P + NW - 1) / NW;
     if (wid == 0 && L < NL) {
-        const int PS = (g.P + NW - 1) / NW;
         const long long NLl = NL;
         reduce_super<R, C>(sm + lane, rs, 32, nw, J == 0, J == PS - 1, srec + (long long)J * RL::REC * NLl + L, NLl);
     }
+    if (counters == nullptr) return;
+    // ---- the last tile of this band group to finish solves the group's
+    //      reduced system (K2) right here: no separate launch, and the solve
+    //      overlaps the remaining tiles of other groups.
+    __shared__ int s_last;
+    __threadfence();  // publish this tile's super-records before counting it
+    __syncthreads();
+    if (wid == 0 && lane == 0) {
+        const int done = atomicAdd(&counters[blockIdx.x], 1);
+        s_last = (done == PS - 1);
+        if (s_last) counters[blockIdx.x] = 0;  // ready for the next pass / replay
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    PassGeom gs = g;
+    gs.P = PS;
+    k2_tree_body<R, C>(gs, srec, rsc, zs, sm, lane, wid, NW, blockIdx.x);
 }
 
 // Interior solve of one chunk with both separators known (zl: previous
@@ -949,38 +976,34 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
         const int n = TR * C;
         const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
-        const int nv = vec ? (n >> 2) : n;      // vectors per column
-        const int per = nv >= 32 ? 1 : 32 / nv;  // columns per warp step
-        const int sub = nv >= 32 ? 0 : lane / nv;
-        const int e0 = nv >= 32 ? lane : lane - sub * nv;
-        for (int xb = wid * per; xb < ncol; xb += NW * per) {
-            const int xl = xb + sub;
-            if (sub >= per || xl >= ncol) continue;
-            const float sc = inv_col[xl];
-            if (sc == 0.f) continue;
-            const float* trow = tl + xl * TP;
-            float* orow = oi + ((long long)(xa + xl) * g.Hl + Y0) * C;
-            // constant-stride loops only: a runtime stride costs an integer
-            // division per column for the trip count
+        const int nv = vec ? (n >> 2) : n;  // vectors per output column
+        // Thread tid owns vector slot e of columns c0, c0 + cps, ...: one
+        // division per thread, then pointer increments.
+        const int cps = nv <= NT ? NT / nv : 1;  // columns per CTA step
+        const int c0 = nv <= NT ? tid / nv : 0;
+        const int e = tid - c0 * nv;
+        if (c0 < cps && e < nv) {
+            const long long ostep = (long long)cps * g.Hl * C;
+            float* op = oi + ((long long)(xa + c0) * g.Hl + Y0) * C;
+            const float* tp = tl + c0 * TP;
             if (vec) {
-                auto put4 = [&](int e4) {
-                    float4 v = reinterpret_cast<const float4*>(trow)[e4];
-                    v.x *= sc;
-                    v.y *= sc;
-                    v.z *= sc;
-                    v.w *= sc;
-                    reinterpret_cast<float4*>(orow)[e4] = v;
-                };
-                if (nv <= 32) {
-                    if (e0 < nv) put4(e0);
-                } else {
-                    for (int e4 = lane; e4 < nv; e4 += 32) put4(e4);
+                for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
+                    const float sc = inv_col[xl];
+                    if (sc == 0.f) continue;
+                    for (int e4 = e; e4 < nv; e4 += NT) {
+                        float4 v = reinterpret_cast<const float4*>(tp)[e4];
+                        v.x *= sc;
+                        v.y *= sc;
+                        v.z *= sc;
+                        v.w *= sc;
+                        reinterpret_cast<float4*>(op)[e4] = v;
+                    }
                 }
             } else {
-                if (nv <= 32) {
-                    if (e0 < nv) orow[e0] = trow[e0] * sc;
-                } else {
-                    for (int e2 = lane; e2 < nv; e2 += 32) orow[e2] = trow[e2] * sc;
+                for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
+                    const float sc = inv_col[xl];
+                    if (sc == 0.f) continue;
+                    for (int e2 = e; e2 < nv; e2 += NT) op[e2] = tp[e2] * sc;
                 }
             }
         }
@@ -1023,15 +1046,19 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
     const int PS = (g.P + NW - 1) / NW;
     cudaError_t e;
     if (PS > 1) {
+        const bool fuse = tile_fuse_k2(PS) && pl.counters != nullptr;
         {
             ProfScope ps("ka_tile", st);
-            const size_t smem = (size_t)RL::REC * (NW * 32 + 1) * sizeof(float);
+            const size_t smem_ka = (size_t)RL::REC * (NW * 32 + 1) * sizeof(float);
+            const size_t smem_k2 = fuse ? k2_tree_smem<R, C>(NW) : 0;
+            const size_t smem = smem_ka > smem_k2 ? smem_ka : smem_k2;
             e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            ka_tile<R, C, CG><<<dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st>>>(g, pl.src, pl.guid, pl.rec, *pl.w);
+            ka_tile<R, C, CG><<<dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st>>>(
+                g, pl.src, pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, *pl.w);
         }
-        {
-            ProfScope ps("k2_reduced", st);
+        if (!fuse) {
+            ProfScope ps("k2_tree", st);
             PassGeom gs = g;
             gs.P = PS;
             const int NG = PS >= 64 ? 16 : 8;
