@@ -56,6 +56,10 @@ def parse():
     p.add_argument("--no-graph", action="store_true", help="launch kernels individually instead of graph replay")
     p.add_argument("--no-prof", action="store_true", help="no per-launch events (no kernel breakdown / roofline)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--sharded", action="store_true",
+                   help="line-slab shard ONE image over the ranks (default for c5 at N>1)")
+    p.add_argument("--local-shards", type=int, default=1,
+                   help="with --sharded at N=1: run this many shards in one process (validation)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline sample budget")
     return p.parse_args()
 
@@ -70,7 +74,7 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def config_block(wl: WL.Workload, n: int, batch_per_rank: int) -> dict:
+def config_block(wl: WL.Workload, n: int, batch_per_rank: int, sharded: bool = False, shards: int = 1) -> dict:
     c = wl.cfg
     return {
         "workload": f"{wl.name}: {wl.width}x{wl.height}x{wl.channels}"
@@ -83,7 +87,8 @@ def config_block(wl: WL.Workload, n: int, batch_per_rank: int) -> dict:
         "guidance": "luminance" if wl.name == "c2" else ("per-pair voronoi" if wl.sparse else "input"),
         "l2": "flushed between timed steps (256 MiB memset)",
         "launch": "CUDA graph replay per filter (captured once, SGWLS_B200_GRAPH)",
-        "parallelism": ("batch-shard" if wl.sparse else "replicas") + f" x{n}",
+        "parallelism": (f"line-slab shards x{shards} (NCCL all-to-all transpose between passes)" if sharded else
+                        ("batch-shard" if wl.sparse else "replicas") + f" x{n}"),
     }
 
 
@@ -181,8 +186,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    sharded = (not wl.sparse) and (args.sharded or (world > 1 and wl.name == "c5"))
     # ---- inputs for this rank
-    if wl.sparse:
+    if sharded:
+        from paper_1705_01674_b200.sharded import DistExchange, LocalExchange, ShardedSmoother
+
+        ht, hg = WL.GENERATORS[wl.name](0)  # ONE image, cut into windows
+        ex = DistExchange() if world > 1 else LocalExchange(args.local_shards)
+        sm = ShardedSmoother(wl.height, wl.width, wl.channels, 1, wl.cfg, exchange=ex)
+        sm.load(ht, hg)
+        batch_per_rank = 1
+        px_step = wl.width * wl.height // world  # whole-image pixels per step, shared by the ranks
+        scaling = "strong"
+        dout = None
+    elif wl.sparse:
         per = max(1, wl.batch // world)
         ids = list(range(rank * per, rank * per + per))
         trip = [WL.gen_c4(i) for i in ids]
@@ -210,7 +227,9 @@ def main():
     use_graph = not args.no_graph
 
     def step():
-        if wl.sparse:
+        if sharded:
+            sm.run()
+        elif wl.sparse:
             S.interpolate_sparse_device(dv, dm, dg, cfg, out=dout, stream=stream, graph=use_graph)
         else:
             S.smooth_device(dt, dg, cfg, out=dout, stream=stream, graph=use_graph)
@@ -218,7 +237,7 @@ def main():
     # correctness gate of this very configuration (cheap, outside timing)
     step()
     torch.cuda.synchronize()
-    if not bool(torch.isfinite(dout).all()):
+    if not bool(torch.isfinite(sm.owned()[2] if sharded else dout).all()):
         raise SystemExit("non-finite output")
 
     sampler = ClockSampler(local)
@@ -279,6 +298,8 @@ def main():
     peak, peak_src = peaks()
     c_rhs = wl.channels + (1 if wl.sparse else 0)
     pass_bytes = batch_per_rank * 4 * wl.width * wl.height * (2 * c_rhs + 1)
+    if sharded:
+        pass_bytes //= world  # this GPU's share of the image (window halos not counted)
     T = cfg.iterations
     pass_ms = total_ms / args.steps / T
     achieved = pass_bytes / (pass_ms / 1e3) / 1e9
@@ -293,13 +314,14 @@ def main():
                 traffic = json.load(f).get("dram_bytes_per_pass")
         except Exception:
             traffic = None
-    filter_bytes = wl.bytes_alg() * batch_per_rank // wl.batch
+    filter_bytes = wl.bytes_alg() * batch_per_rank // wl.batch // (world if sharded else 1)
     roofline = {
         "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
         "achieved": achieved, "frac": achieved / peak, "traffic": traffic,
-        "launch_unit": "one directional pass: ka_tile (chunk spike-forward + in-tile reduction) + k2_reduced "
-                       "(super-separator solve) + kb_tile (interior solve + averaging + transposed store); "
-                       "duration = timed step / T",
+        "launch_unit": "one directional pass: ka_tile (chunk spike-forward + in-tile reduction; solves the "
+                       "reduced system itself when short) [+ k2_tree (super-separator solve)] + kb_tile (interior "
+                       "solve + averaging + transposed store); duration = timed step / T"
+                       + ("; sharded: includes the all-to-all transpose" if sharded else ""),
         "bytes_alg_per_pass": pass_bytes, "pass_ms": pass_ms,
         "dominant_kernel": dominant,
         "dominant_share": (kern[dominant]["ms"] / kern_total) if dominant else None,
@@ -309,12 +331,16 @@ def main():
     }
     kernels = {k: {"launches_per_step": v["launches"] / psteps, "ms_per_step_instrumented": v["ms"] / psteps,
                    "share": v["ms"] / kern_total} for k, v in kern.items()}
-    launches = S.kernel_launches(wl.width, wl.height, wl.channels, 1, batch_per_rank, wl.sparse, cfg)
+    if sharded:
+        launches = sm.kernel_launches()
+    else:
+        launches = S.kernel_launches(wl.width, wl.height, wl.channels, 1, batch_per_rank, wl.sparse, cfg)
 
     # ---- e2e through the host-pointer C ABI from pinned buffers
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_leg(args, wl, cfg, world, rank, dist if world > 1 else None)
+        e2e = (e2e_sharded(args, wl, sm, ht, hg, world) if sharded else
+               e2e_leg(args, wl, cfg, world, rank, dist if world > 1 else None))
 
     # ---- CPU baseline (rank 0, N=1)
     cpu = None
@@ -330,7 +356,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": DATA,
-            "config": config_block(wl, world, batch_per_rank),
+            "config": config_block(wl, world, batch_per_rank, sharded, sm.G if sharded else 1),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * args.steps,
             "clocks": clocks, "kernels_instrumented": kernels,
             "step_ms_median": statistics.median(step_ms),
@@ -399,6 +425,42 @@ def e2e_leg(args, wl, cfg, world, rank, dist):
     return {"value": world * px * steps / el / 1e6, "unit": "MPix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": el / steps * 1e3,
             "api": "sgwls_b200_interpolate_sparse_batch" if wl.sparse else "sgwls_b200_smooth (host pointers, pinned)"}
+
+
+def e2e_sharded(args, wl, sm, ht, hg, world):
+    """Sharded e2e: every step uploads this rank's pinned input windows, runs the
+    T passes with their exchanges and reads back the rows this rank owns."""
+    import torch
+    import torch.distributed as dist
+
+    wins = sm.host_windows(ht, hg)
+    rows = [sm.owned(g)[2] for g in sm.ex.local]
+    hout = [torch.empty(r.shape, dtype=torch.float32).pin_memory() for r in rows]
+    h2d = sm.window_bytes()
+    d2h = sum(4 * r.numel() for r in rows)
+
+    def call():
+        sm.load_windows(wins)
+        sm.run()
+        for r, o in zip(rows, hout):
+            o.copy_(r, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+
+    for _ in range(max(1, args.warmup)):
+        call()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    el = time.perf_counter() - t0
+    if world > 1:
+        tt = torch.tensor([el], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    return {"value": wl.width * wl.height * args.steps / el / 1e6, "unit": "MPix/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": el / args.steps * 1e3,
+            "api": "ShardedSmoother.load_windows + run + owned rows D2H (pinned host buffers)"}
 
 
 def reference_arm(args, wl, rank, world):

@@ -91,6 +91,16 @@ int sgwls_b200_smooth_device(const float* d_targets, const float* d_guidances, i
                              int channels, int guidance_channels, const sgwls_b200_config* cfg, float* d_out,
                              void* stream, int flags, char* err, size_t errlen);
 
+/* ONE Column-axis pass (proj/src/smoother.cpp:51-99, run_pass with Axis::Column;
+ * cfg->iterations and cfg->first_axis are ignored) on device buffers.  The output
+ * is written TRANSPOSED: d_out_t[b][x][y][c] = pass(d_src)[b][y][x][c], i.e. a
+ * height-wide, width-tall image ready to be the next (Row-axis) pass's input.
+ * Building block of the line-slab sharded filter (paper_1705_01674_b200/sharded.py,
+ * BASELINE c5 "lines sharded across GPUs"); same flags as smooth_device. */
+int sgwls_b200_pass_device(const float* d_src, const float* d_guidances, int batch, int width, int height,
+                           int channels, int guidance_channels, const sgwls_b200_config* cfg, float* d_out_t,
+                           void* stream, int flags, char* err, size_t errlen);
+
 /* sgwls::interpolate_sparse on host buffers (synchronous).  values: width*height*channels,
  * mask: width*height (0/1), out: like values, undefined_mask: width*height or NULL. */
 int sgwls_b200_interpolate_sparse(const float* values, const float* mask, int width, int height, int channels,

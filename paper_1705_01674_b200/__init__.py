@@ -4,8 +4,9 @@ kernels behind a C ABI (include/sgwls_b200.h).  See DESIGN.md."""
 from .config import (Axis, CudaError, Error, SmoothConfig, SparseField, WeightKind, WeightParams,  # noqa: F401
                      orthogonal)
 from .api import (interpolate_sparse, interpolate_sparse_batch, interpolate_sparse_device,  # noqa: F401
-                  kernel_launches, smooth, smooth_batch, smooth_device, validate, version)
+                  kernel_launches, pass_device, smooth, smooth_batch, smooth_device, validate, version)
 
 __all__ = ["Axis", "CudaError", "Error", "SmoothConfig", "SparseField", "WeightKind", "WeightParams",
            "orthogonal", "smooth", "smooth_batch", "smooth_device", "interpolate_sparse",
-           "interpolate_sparse_batch", "interpolate_sparse_device", "validate", "kernel_launches", "version"]
+           "interpolate_sparse_batch", "interpolate_sparse_device", "validate", "kernel_launches", "version",
+           "pass_device"]

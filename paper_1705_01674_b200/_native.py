@@ -58,6 +58,8 @@ SIGNATURES = {
                                           C.POINTER(NativeConfig), _P, C.c_char_p, C.c_size_t]),
     "sgwls_b200_smooth_device": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                            C.POINTER(NativeConfig), _P, _P, C.c_int, C.c_char_p, C.c_size_t]),
+    "sgwls_b200_pass_device": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(NativeConfig), _P, _P, C.c_int, C.c_char_p, C.c_size_t]),
     "sgwls_b200_interpolate_sparse": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, _P, C.c_int,
                                                 C.POINTER(NativeConfig), _P, _P, C.c_char_p, C.c_size_t]),
     "sgwls_b200_interpolate_sparse_batch": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,

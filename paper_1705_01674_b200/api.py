@@ -167,6 +167,29 @@ def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, s
     return out
 
 
+def pass_device(src, guidance, cfg: SmoothConfig | None = None, out=None, stream=None, sync: bool = False,
+                graph: bool = False):
+    """ONE Column-axis pass (proj/src/smoother.cpp:51-99) on torch CUDA tensors (H,W[,C]) or (B,H,W,C),
+    written transposed: returns (W,H[,C]) / (B,W,H,C).  cfg.iterations / cfg.first_axis are ignored."""
+    import torch
+
+    cfg = cfg or SmoothConfig()
+    b, h, w, c = _dev_dims(src, "pass")
+    bg, hg, wg, gc = _dev_dims(guidance, "pass")
+    if (hg, wg) != (h, w) or bg != b:
+        raise Error("smooth: target and guidance dimensions differ")
+    if out is None:
+        shape = (w, h) if src.dim() == 2 else ((w, h, c) if src.dim() == 3 else (b, w, h, c))
+        out = torch.empty(shape, dtype=torch.float32, device=src.device)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    flags = (N.SYNC if sync else 0) | (N.GRAPH if graph else 0)
+    rc = N.lib().sgwls_b200_pass_device(src.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
+                                        out.data_ptr(), _stream_ptr(stream), flags, err, len(err))
+    N.check(rc, err)
+    return out
+
+
 def interpolate_sparse_device(values, masks, guidances, cfg: SmoothConfig | None = None, out=None,
                               undefined=None, stream=None, sync: bool = False, validate: bool = False,
                               graph: bool = False):

@@ -296,12 +296,16 @@ void require_device() {
 
 // The T-pass pipeline on device buffers (proj/src/smoother.cpp:113-125).
 // Returns after enqueueing; *d_err receives the first-pass NaN-weight report.
+// pass_only: exactly one Column-axis pass (proj/src/smoother.cpp:51-99) whose
+// output is written in the transposed layout (the building block of the
+// line-slab sharded filter, sharded.py).
 void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int C, int Cg,
-                const sgwls_b200_config* cfg, float* d_out, unsigned long long* d_err, cudaStream_t st) {
+                const sgwls_b200_config* cfg, float* d_out, unsigned long long* d_err, cudaStream_t st,
+                bool pass_only = false) {
     WeightDev wd;
     build_weights(cfg, wd);
-    const int T = cfg->iterations;
-    const int fa = cfg->first_axis;
+    const int T = pass_only ? 1 : cfg->iterations;
+    const int fa = pass_only ? 0 : cfg->first_axis;
     const bool need0 = (fa == 0) || T >= 2;
     const bool need1 = (fa == 1) || T >= 2;
     AxisPlan ap0 = plan_axis(H, W, C, Cg, cfg->r, cfg->tau, batch);  // column passes
@@ -359,7 +363,7 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.src = src;
         pl.guid = o == 0 ? d_g : gt.p;
         const bool lastp = (p == T - 1);
-        pl.transpose_out = lastp ? (o == 1) : 1;
+        pl.transpose_out = (lastp && !pass_only) ? (o == 1) : 1;
         float* out = d_out;
         if (!lastp) {  // never overwrite the pass input
             const int out_idx = (src_idx == 0) ? 1 : 0;
@@ -595,6 +599,32 @@ int sgwls_b200_smooth_device(const float* d_t, const float* d_g, int batch, int 
         }
         ErrWord ew(st);
         run_smooth(d_t, d_g, batch, width, height, channels, gch, cfg, d_out, ew.d, st);
+        if (flags & SGWLS_B200_SYNC) finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_pass_device(const float* d_src, const float* d_g, int batch, int width, int height, int channels,
+                           int gch, const sgwls_b200_config* cfg, float* d_out_t, void* stream, int flags,
+                           char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(batch, width, height, channels, gch, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        cudaStream_t st = (cudaStream_t)stream;
+        if (flags & SGWLS_B200_GRAPH) {
+            const void* ptrs[3] = {d_src, d_g, d_out_t};
+            const int dims[5] = {batch, width, height, channels, gch};
+            run_graphed(graph_key(ptrs, 3, dims, 5, cfg, 2), st, flags & SGWLS_B200_SYNC,
+                        [&](cudaStream_t gs, unsigned long long* de) {
+                            run_smooth(d_src, d_g, batch, width, height, channels, gch, cfg, d_out_t, de, gs, true);
+                        });
+            return;
+        }
+        ErrWord ew(st);
+        run_smooth(d_src, d_g, batch, width, height, channels, gch, cfg, d_out_t, ew.d, st, true);
         if (flags & SGWLS_B200_SYNC) finish_sync(ew.d, st);
     });
 }
