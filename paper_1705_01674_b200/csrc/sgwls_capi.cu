@@ -145,7 +145,7 @@ struct AxisPlan {
     int kmax;
     int bx;
     int fast, step, ncta, nw, nph;
-    size_t rec_n, rs_n, z_n, u_n;
+    size_t rec_n, rs_n, z_n, u_n, crec_n = 0;
 };
 
 
@@ -161,6 +161,7 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
     g.Cg = Cg;
     g.r = r;
     g.tau = tau;
+    g.tau_mul = tau_multiplier(tau);
     g.batch = batch;
     if (Wl < 2 * r + 1) {
         g.degenerate = 1;
@@ -227,6 +228,7 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         }
         ap.nph = nph;
         ap.rec_n = PS > 1 ? (size_t)PS * rec_floats(r, C) * NL : 0;
+        ap.crec_n = PS > 1 ? (size_t)P * rec_floats(r, C) * NL : 0;
         ap.rs_n = PS > 1 ? (size_t)(PS - 1) * r * rs_floats(r, C) * NL : 0;
         ap.z_n = PS > 1 ? (size_t)(PS - 1) * r * C * NL : 0;
         ap.u_n = 0;
@@ -256,7 +258,8 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
 int kernels_per_pass(const AxisPlan& ap) {
     if (ap.fast) {  // ka_tile (K2 fused or its own k2_tree), kb_tile
         const int PS = (ap.g.P + ap.nw - 1) / ap.nw;
-        return (PS > 1 ? (tile_fuse_k2(PS) ? 1 : 2) : 0) + 1;
+        static const int fuse_k2 = std::getenv("SGWLS_FUSE_K2") ? std::atoi(std::getenv("SGWLS_FUSE_K2")) : 0;
+        return (PS > 1 ? ((fuse_k2 && tile_fuse_k2(PS)) ? 1 : 2) : 0) + 1;
     }
     return (ap.g.P > 1 ? 2 : 0) + 2;
 }
@@ -311,22 +314,25 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
     AxisPlan ap0 = plan_axis(H, W, C, Cg, cfg->r, cfg->tau, batch);  // column passes
     AxisPlan ap1 = plan_axis(W, H, C, Cg, cfg->r, cfg->tau, batch);  // row passes (transposed layout)
     auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
-    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0;
+    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0, crec_n = 0;
     if (need0) {
         rec_n = mx(rec_n, ap0.rec_n);
+        crec_n = mx(crec_n, ap0.crec_n);
         rs_n = mx(rs_n, ap0.rs_n);
         z_n = mx(z_n, ap0.z_n);
         u_n = mx(u_n, ap0.u_n);
     }
     if (need1) {
         rec_n = mx(rec_n, ap1.rec_n);
+        crec_n = mx(crec_n, ap1.crec_n);
         rs_n = mx(rs_n, ap1.rs_n);
         z_n = mx(z_n, ap1.z_n);
         u_n = mx(u_n, ap1.u_n);
     }
     const size_t img_n = (size_t)batch * W * H * C;
     const size_t ngroups = (size_t)(mx(ap0.g.nb, ap1.g.nb) * batch + 31) / 32;
-    DevBuf rec, rs, z, U, bufA, bufB, gt, cnt;
+    DevBuf rec, rs, z, U, bufA, bufB, gt, cnt, crec;
+    crec.alloc(crec_n, st);
     cnt.alloc(ngroups, st);
     CK(cudaMemsetAsync(cnt.p, 0, ngroups * sizeof(float), st));
     rec.alloc(rec_n, st);
@@ -359,7 +365,14 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.ncta = ap.ncta;
         pl.nw = ap.nw;
         pl.nph = ap.nph;
-        pl.counters = reinterpret_cast<int*>(cnt.p);
+        static const int fuse_k2 = [] {
+            // tuning knob: 1 = the last KA tile of a band group solves short reduced
+            // systems in place (measured neutral to -2% on B200, so off by default)
+            const char* v = std::getenv("SGWLS_FUSE_K2");
+            return v ? std::atoi(v) : 0;
+        }();
+        pl.counters = fuse_k2 ? reinterpret_cast<int*>(cnt.p) : nullptr;
+        pl.crec = crec.p;
         pl.src = src;
         pl.guid = o == 0 ? d_g : gt.p;
         const bool lastp = (p == T - 1);

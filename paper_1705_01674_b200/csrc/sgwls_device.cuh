@@ -51,7 +51,16 @@ struct PassGeom {
     long long n;       // positions per band = m*Hl
     long long img_stride;   // floats per image of the target layout (Hl*Wl*C)
     long long gimg_stride;  // floats per image of the guidance layout
+    unsigned tau_mul;       // ceil(2^32 / tau) (tau > 1): exact x / tau for 0 <= x < 2^28
 };
+
+__host__ __device__ __forceinline__ unsigned tau_multiplier(int tau) {
+    return tau > 1 ? (unsigned)(0xffffffffu / (unsigned)tau) + 1u : 0u;
+}
+
+__device__ __forceinline__ int div_tau(const PassGeom& g, int x) {
+    return g.tau == 1 ? x : (int)__umulhi((unsigned)x, g.tau_mul);
+}
 
 __host__ __device__ __forceinline__ int band_center(const PassGeom& g, int b) {
     if (g.degenerate) return (g.Wl - 1) / 2;

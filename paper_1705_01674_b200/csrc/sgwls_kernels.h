@@ -27,6 +27,7 @@ struct PassLaunch {
     unsigned long long* err;  // NaN-weight report (first pass only), or nullptr
     const WeightDev* w;
     int* counters = nullptr;  // tiled path: per-band-group tile counters (zeroed; self-resetting)
+    float* crec = nullptr;    // tiled path: every chunk's record (KA -> KB), [chunk][field][line]
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);

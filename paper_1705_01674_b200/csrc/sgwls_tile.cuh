@@ -124,7 +124,9 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
     // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time.
     // A NaN weight (NaN guidance) is the reference's "non-positive pivot" failure:
     // remember the first offending position and report it once.
-    int bad = 0x7fffffff;
+    // Cheap detection (one add per edge: any NaN poisons the sum; weights are
+    // finite and >= 0 otherwise), exact location only on the rare slow path.
+    float acc = 0.f;
 #pragma unroll
     for (int k = 0; k < K; ++k) {
 #pragma unroll
@@ -138,12 +140,20 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
             }
             const float wv = guidance_weight(W, r2, edge_d2(k % M, t));
             in.w[k][t - 1] = wv;
-            const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
-            bad = (!(wv >= 0.f) && exists) ? min(bad, y0 * M + k - t) : bad;
+            acc += wv;
         }
     }
-    if (err != nullptr && bad != 0x7fffffff)
-        atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)bad);
+    if (err != nullptr && !(acc >= 0.f)) {
+        int bad = 0x7fffffff;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int t = 1; t <= R; ++t) {
+                const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
+                bad = (!(in.w[k][t - 1] >= 0.f) && exists) ? min(bad, y0 * M + k - t) : bad;
+            }
+        if (bad != 0x7fffffff) atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)bad);
+    }
 }
 
 // ------------------------------------------------- elimination window (scalar)
@@ -594,7 +604,10 @@ __device__ __forceinline__ void solve_inner(const float* recs, long long rs, lon
 // Body of the tree solve for one group of 32 lines (lane = line, w = warp),
 // usable both as its own kernel and from the last KA tile of a band group.
 template <int R, int C>
-__device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* __restrict__ rec,
+// `rec` is deliberately not __restrict__: in the fused form the records were
+// written by other CTAs of the same launch, so they must not be read through
+// the non-coherent (LDG.CONSTANT) path.
+__device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec,
                                              float* __restrict__ rsc, float* __restrict__ z, float* sm, int lane,
                                              int w, int NG, int group) {
     using RL = Rec<R, C>;
@@ -662,7 +675,8 @@ template <int R, int C, int CG>
 __global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
                                                float* __restrict__ rsc, float* __restrict__ zs,
-                                               int* __restrict__ counters, const __grid_constant__ WeightDev W) {
+                                               int* __restrict__ counters, float* __restrict__ crec,
+                                               const __grid_constant__ WeightDev W) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1;
     using RL = Rec<R, C>;
@@ -684,6 +698,10 @@ __global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows,
                                  nullptr, L);
         chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0, j == g.P - 1, nrows * M, rec, rs);
+        // every chunk record also goes to HBM for KB (saves KB a spike-forward)
+        float* dst = crec + (long long)j * RL::REC * NL + L;
+#pragma unroll
+        for (int f = 0; f < RL::REC; ++f) dst[(long long)f * NL] = rec[f * rs];
     }
     __syncthreads();
     const int PS = (g.P + NW - 1) / NW;
@@ -804,8 +822,8 @@ struct TileOut {
 __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, int& bmax) {
     const int r = g.r, tau = g.tau;
     const int lo_b = x - 2 * r;
-    int b0 = lo_b <= 0 ? 0 : (lo_b + tau - 1) / tau;
-    int b1 = x / tau;
+    int b0 = lo_b <= 0 ? 0 : div_tau(g, lo_b + tau - 1);
+    int b1 = div_tau(g, x);
     if (b1 > g.nreg - 1) b1 = g.nreg - 1;
     bmin = b0;
     bmax = b1;
@@ -818,7 +836,8 @@ __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, in
 template <int R, int C, int CG>
 __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, const float* __restrict__ zs,
-                                               const TileOut to, unsigned long long* __restrict__ err,
+                                               const float* __restrict__ crec, const TileOut to,
+                                               unsigned long long* __restrict__ err,
                                                const __grid_constant__ WeightDev W) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1, K = RW * M, NF = R + C;
@@ -860,7 +879,13 @@ __global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __
     if (active) {
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
                                  L);
-        chunk_spike_forward<R, C, CG, RW>(in, lam, j > 0, j == g.P - 1, nrows * M, recs + tid, rs);
+        if (crec != nullptr) {  // KA's record of this chunk
+            const float* srcr = crec + (long long)j * RL::REC * NLl + L;
+#pragma unroll
+            for (int f = 0; f < RL::REC; ++f) recs[f * rs + tid] = srcr[(long long)f * NLl];
+        } else {
+            chunk_spike_forward<R, C, CG, RW>(in, lam, j > 0, j == g.P - 1, nrows * M, recs + tid, rs);
+        }
     }
     __syncthreads();
 
@@ -1055,7 +1080,7 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
             ka_tile<R, C, CG><<<dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st>>>(
-                g, pl.src, pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, *pl.w);
+                g, pl.src, pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w);
         }
         if (!fuse) {
             ProfScope ps("k2_tree", st);
@@ -1076,8 +1101,8 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph};
-        kb_tile<R, C, CG><<<dim3(pl.ncta, PS, g.batch), dim3(32, NW), smem, st>>>(g, pl.src, pl.guid, pl.z, to,
-                                                                                 pl.err, *pl.w);
+        kb_tile<R, C, CG><<<dim3(pl.ncta, PS, g.batch), dim3(32, NW), smem, st>>>(
+            g, pl.src, pl.guid, pl.z, PS > 1 ? pl.crec : nullptr, to, pl.err, *pl.w);
     }
     return cudaGetLastError();
 }

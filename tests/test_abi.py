@@ -135,6 +135,4 @@ def test_chunking_invariants(extent, sweep, r, tau):
 def test_kernel_launch_accounting():
     cfg = S.SmoothConfig(lambda_=400.0, r=1, tau=3, iterations=4)
     n = S.kernel_launches(1920, 1080, 3, 1, 1, False, cfg)
-    # guidance transpose + 2 passes over 1080-row lines (KA with fused K2, KB)
-    # + 2 passes over 1920-row lines (KA, K2 tree, KB)
-    assert n == 1 + 2 * 2 + 2 * 3
+    assert n == 1 + 4 * 3  # guidance transpose + 4 passes x (KA, K2 tree, KB)
