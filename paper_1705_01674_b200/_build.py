@@ -44,8 +44,8 @@ def _stale(target: str, sources: list[str]) -> bool:
     return any(os.path.getmtime(s) > t for s in sources if os.path.exists(s))
 
 
-def _compile(src: str, extra: list[str]) -> str:
-    obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
+def _compile(src: str, extra: list[str], obj_dir: str = OBJ) -> str:
+    obj = os.path.join(obj_dir, os.path.basename(src).replace(".cu", ".o"))
     if _stale(obj, [src] + _deps()):
         cmd = [nvcc()] + ARCH + NVCC_FLAGS + extra + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -54,21 +54,32 @@ def _compile(src: str, extra: list[str]) -> str:
     return obj
 
 
-def build_native(verbose: bool = False, extra: list[str] | None = None) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build_native(verbose: bool = False, extra: list[str] | None = None, variant: str | None = None) -> str:
+    """variant: build a tuning variant (extra nvcc flags) into variants/lib_<variant>.so
+    (load it with SGWLS_B200_LIB=...); the default build is libsgwls_b200.so."""
+    obj_dir = OBJ if variant is None else os.path.join(ROOT, "build", "obj_" + variant)
+    lib = LIB if variant is None else os.path.join(PKG, "variants", f"lib_{variant}.so")
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     extra = list(extra or [])
     with cf.ThreadPoolExecutor(max_workers=max(2, os.cpu_count() or 2)) as ex:
-        objs = list(ex.map(lambda s: _compile(s, extra), srcs))
-    if _stale(LIB, objs):
-        cmd = [nvcc()] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart"]
+        objs = list(ex.map(lambda s: _compile(s, extra, obj_dir), srcs))
+    if _stale(lib, objs):
+        cmd = [nvcc()] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     if verbose:
-        print("built", LIB)
-    return LIB
+        print("built", lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build_native(verbose=True)
+    import sys
+
+    args = sys.argv[1:]
+    var = None
+    if args and args[0] == "--variant":
+        var, args = args[1], args[2:]
+    build_native(verbose=True, extra=args, variant=var)

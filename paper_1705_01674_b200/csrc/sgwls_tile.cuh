@@ -672,7 +672,19 @@ __host__ inline size_t k2_tree_smem(int NG) {
 // ===================================================================== KA
 
 template <int R, int C, int CG>
-__global__ void __launch_bounds__(256) ka_tile(const PassGeom g, const float* __restrict__ src,
+// Register budgets: plain __launch_bounds__(256) (ptxas settles at ~80-128
+// registers) measured best overall on B200; tuning variants override these.
+#ifdef SGWLS_KA_MINB
+#define SGWLS_KA_BOUNDS __launch_bounds__(256, SGWLS_KA_MINB)
+#else
+#define SGWLS_KA_BOUNDS __launch_bounds__(256)
+#endif
+#ifdef SGWLS_KB_MINB
+#define SGWLS_KB_BOUNDS __launch_bounds__(256, SGWLS_KB_MINB)
+#else
+#define SGWLS_KB_BOUNDS __launch_bounds__(256)
+#endif
+__global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
                                                float* __restrict__ rsc, float* __restrict__ zs,
                                                int* __restrict__ counters, float* __restrict__ crec,
@@ -834,7 +846,7 @@ __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, in
 }
 
 template <int R, int C, int CG>
-__global__ void __launch_bounds__(256) kb_tile(const PassGeom g, const float* __restrict__ src,
+__global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, const float* __restrict__ zs,
                                                const float* __restrict__ crec, const TileOut to,
                                                unsigned long long* __restrict__ err,
