@@ -4,6 +4,7 @@ rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[0]
+units = rows[1]
 keys = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
@@ -16,7 +17,7 @@ for r in rows[2:]:
     print("==", name)
     for k in keys:
         if k in hdr:
-            print("   ", k, r[hdr.index(k)])
+            print("   ", k, r[hdr.index(k)], units[hdr.index(k)])
     st = []
     for i, h in enumerate(hdr):
         if h.startswith("smsp__pcsamp_warps_issue_stalled_") and not h.endswith("not_issued"):

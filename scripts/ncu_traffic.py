@@ -1,0 +1,30 @@
+"""DRAM bytes of one pass (ka_tile + k2_tree + kb_tile, one launch each) from an
+ncu --set full report -> profiles/ncu_traffic_<cfg>.json (read by bench.py)."""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep, cfg = sys.argv[1], sys.argv[2]
+out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(out)))
+hdr, units = rows[0], rows[1]
+scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+seen, total, per = set(), 0.0, {}
+for r in rows[2:]:
+    name = r[hdr.index("Kernel Name")].split("(")[0].replace("void ", "")
+    base = name.split("<")[0]
+    if base in seen:
+        continue
+    seen.add(base)
+    b = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = hdr.index(k)
+        b += float(r[i].replace(",", "")) * scale[units[i]]
+    per[name] = b
+    total += b
+res = {"config": cfg, "report": rep, "dram_bytes_per_pass": total, "per_kernel": per,
+       "note": "ncu --set full, one launch of each pass kernel (cold L2 between replays)"}
+json.dump(res, open(f"profiles/ncu_traffic_{cfg}.json", "w"), indent=1)
+print(json.dumps(res, indent=1))
