@@ -31,6 +31,9 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "sgwls_device.cuh"
 #include "sgwls_kernels.h"
 #include "sgwls_profile.h"
@@ -38,6 +41,38 @@
 
 namespace sgwls_b200 {
 namespace tile {
+
+// Programmatic dependent launch: a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; griddepcontrol.wait blocks until the predecessor grid has
+// completed and its memory is visible (a no-op for ordinary launches).
+// launch_dependents lets the successor start launching.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("SGWLS_PDL");  // tuning knob: 0 = ordinary stream-ordered launches
+        return v ? std::atoi(v) != 0 : true;
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 template <int R, int C>
 struct Rec {
@@ -660,6 +695,8 @@ template <int R, int C>
 __global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __restrict__ rec,
                                                float* __restrict__ rsc, float* __restrict__ z) {
     extern __shared__ float sm[];
+    pdl_wait();     // KA's records
+    pdl_trigger();  // KB may launch now: everything it reads before its own wait (KA's output) is complete
     k2_tree_body<R, C>(g, rec, rsc, z, sm, threadIdx.x, threadIdx.y, blockDim.y, blockIdx.x);
 }
 
@@ -701,6 +738,8 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     const int nw = min(NW, g.P - J * NW);
     const int rs = NW * 32 + 1;  // smem record field stride
     float* rec = sm + wid * 32 + lane;
+    pdl_wait();  // the pass input is the previous pass's output
+    pdl_trigger();
     if (L < NL && wid < nw) {
         const int img = L / g.nb, b = L - img * g.nb;
         const int lo = band_lo(g, b);
@@ -888,6 +927,10 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int y0 = j * RW;
     const int nrows = active ? min(RW, g.Hl - y0) : 0;
     const int lo = active ? band_lo(g, b) : 0;
+    // With chunk records (KA + K2 ran) everything up to the separators is
+    // already complete when this grid may launch (K2 triggers after its own
+    // wait); without them the pass input comes straight from the predecessor.
+    if (crec == nullptr) pdl_wait();
     if (active) {
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
                                  L);
@@ -899,6 +942,8 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             chunk_spike_forward<R, C, CG, RW>(in, lam, j > 0, j == g.P - 1, nrows * M, recs + tid, rs);
         }
     }
+    if (crec != nullptr) pdl_wait();  // K2's separators
+    pdl_trigger();
     __syncthreads();
 
     // ---- 2. lane-per-band solve of the tile's inner separators with the two
@@ -1091,8 +1136,9 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             const size_t smem = smem_ka > smem_k2 ? smem_ka : smem_k2;
             e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            ka_tile<R, C, CG><<<dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st>>>(
-                g, pl.src, pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w);
+            e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st, g, pl.src, pl.guid,
+                           pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w);
+            if (e != cudaSuccess) return e;
         }
         if (!fuse) {
             ProfScope ps("k2_tree", st);
@@ -1102,7 +1148,9 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             const size_t sm2 = k2_tree_smem<R, C>(NG);
             e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
             if (e != cudaSuccess) return e;
-            k2_tree<R, C><<<(NL + 31) / 32, dim3(32, NG), sm2, st>>>(gs, pl.rec, pl.rs, pl.z);
+            e = launch_pdl(k2_tree<R, C>, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs,
+                           pl.z);
+            if (e != cudaSuccess) return e;
         }
     }
     {
@@ -1113,8 +1161,9 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph};
-        kb_tile<R, C, CG><<<dim3(pl.ncta, PS, g.batch), dim3(32, NW), smem, st>>>(
-            g, pl.src, pl.guid, pl.z, PS > 1 ? pl.crec : nullptr, to, pl.err, *pl.w);
+        e = launch_pdl(kb_tile<R, C, CG>, dim3(pl.ncta, PS, g.batch), dim3(32, NW), smem, st, g, pl.src, pl.guid,
+                       (const float*)pl.z, (const float*)(PS > 1 ? pl.crec : nullptr), to, pl.err, *pl.w);
+        if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
 }
