@@ -144,8 +144,8 @@ struct AxisPlan {
     PassGeom g;
     int kmax;
     int bx;
-    int fast, step, ncta, nw, nph;
-    size_t rec_n, rs_n, z_n, u_n, crec_n = 0;
+    int fast, step, ncta, nw, nph, nwa = 8, kc = 0;
+    size_t rec_n, rs_n, z_n, u_n, crec_n = 0, sep_n = 0;
 };
 
 
@@ -202,7 +202,21 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         const int P = (Hl + RW - 1) / RW;
         g.P = P;
         ap.kmax = RW * g.m;
-        const int PS = (P + ap.nw - 1) / ap.nw;
+        static const int ka_warps_env = [] {
+            const char* v = std::getenv("SGWLS_KA_WARPS");  // tuning knob: chunks per KA tile
+            const int n = v ? std::atoi(v) : 0;
+            return n < 0 ? 0 : (n > 8 ? 8 : n);
+        }();
+        static const int kc_env = [] {
+            const char* v = std::getenv("SGWLS_KC");  // tuning knob: 1/0 force the KC path on/off
+            return v ? std::atoi(v) : -1;
+        }();
+        // measured on B200: r = 1 -> one launch fewer (KB solves its tile's inner
+        // separators), 8-chunk tiles; r >= 2 -> KC, 4-chunk KB tiles and 8-chunk
+        // KA tiles (4 with several right-hand sides)
+        ap.kc = kc_env >= 0 ? kc_env : (r >= 2 ? 1 : 0);
+        ap.nwa = ap.kc ? (ka_warps_env ? ka_warps_env : (C >= 2 ? kTileWarps / 2 : kTileWarps)) : ap.nw;
+        const int PS = (P + ap.nwa - 1) / ap.nwa;
         // halo: widest span of bands covering one column (incl. the forced last centre)
         int hspan = 0;
         for (int x = 0; x < Wl; ++x) {
@@ -227,10 +241,11 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
             if (ok) break;
         }
         ap.nph = nph;
-        ap.rec_n = PS > 1 ? (size_t)PS * rec_floats(r, C) * NL : 0;
-        ap.crec_n = PS > 1 ? (size_t)P * rec_floats(r, C) * NL : 0;
+        ap.rec_n = P > 1 ? (size_t)PS * rec_floats(r, C) * NL : 0;
+        ap.crec_n = P > 1 ? (size_t)P * rec_floats(r, C) * NL : 0;
         ap.rs_n = PS > 1 ? (size_t)(PS - 1) * r * rs_floats(r, C) * NL : 0;
         ap.z_n = PS > 1 ? (size_t)(PS - 1) * r * C * NL : 0;
+        ap.sep_n = (P > 1 && ap.kc) ? (size_t)(P - 1) * r * C * NL : 0;
         ap.u_n = 0;
         return ap;
     }
@@ -257,9 +272,10 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
 
 int kernels_per_pass(const AxisPlan& ap) {
     if (ap.fast) {  // ka_tile (K2 fused or its own k2_tree), kb_tile
-        const int PS = (ap.g.P + ap.nw - 1) / ap.nw;
+        const int PS = (ap.g.P + ap.nwa - 1) / ap.nwa;
         static const int fuse_k2 = std::getenv("SGWLS_FUSE_K2") ? std::atoi(std::getenv("SGWLS_FUSE_K2")) : 0;
-        return (PS > 1 ? ((fuse_k2 && tile_fuse_k2(PS)) ? 1 : 2) : 0) + 1;
+        // ka_tile [+ k2_tree unless fused] [+ kc_inner] when the lines have several chunks; kb_tile
+        return (ap.g.P > 1 ? (1 + (ap.kc ? 1 : 0) + ((PS > 1 && !(fuse_k2 && tile_fuse_k2(PS))) ? 1 : 0)) : 0) + 1;
     }
     return (ap.g.P > 1 ? 2 : 0) + 2;
 }
@@ -314,10 +330,11 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
     AxisPlan ap0 = plan_axis(H, W, C, Cg, cfg->r, cfg->tau, batch);  // column passes
     AxisPlan ap1 = plan_axis(W, H, C, Cg, cfg->r, cfg->tau, batch);  // row passes (transposed layout)
     auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
-    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0, crec_n = 0;
+    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0, crec_n = 0, sep_n = 0;
     if (need0) {
         rec_n = mx(rec_n, ap0.rec_n);
         crec_n = mx(crec_n, ap0.crec_n);
+        sep_n = mx(sep_n, ap0.sep_n);
         rs_n = mx(rs_n, ap0.rs_n);
         z_n = mx(z_n, ap0.z_n);
         u_n = mx(u_n, ap0.u_n);
@@ -325,6 +342,7 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
     if (need1) {
         rec_n = mx(rec_n, ap1.rec_n);
         crec_n = mx(crec_n, ap1.crec_n);
+        sep_n = mx(sep_n, ap1.sep_n);
         rs_n = mx(rs_n, ap1.rs_n);
         z_n = mx(z_n, ap1.z_n);
         u_n = mx(u_n, ap1.u_n);
@@ -333,6 +351,8 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
     const size_t ngroups = (size_t)(mx(ap0.g.nb, ap1.g.nb) * batch + 31) / 32;
     DevBuf rec, rs, z, U, bufA, bufB, gt, cnt, crec;
     crec.alloc(crec_n, st);
+    DevBuf sepb;
+    sepb.alloc(sep_n, st);
     cnt.alloc(ngroups, st);
     CK(cudaMemsetAsync(cnt.p, 0, ngroups * sizeof(float), st));
     rec.alloc(rec_n, st);
@@ -364,6 +384,9 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.step = ap.step;
         pl.ncta = ap.ncta;
         pl.nw = ap.nw;
+        pl.nwa = ap.nwa;
+        pl.kc = ap.kc;
+        pl.sep = sepb.p;
         pl.nph = ap.nph;
         static const int fuse_k2 = [] {
             // tuning knob: 1 = the last KA tile of a band group solves short reduced

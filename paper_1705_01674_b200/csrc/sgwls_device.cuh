@@ -78,8 +78,13 @@ __host__ __device__ __forceinline__ int chunk_row(const PassGeom& g, int j) {
 
 // Rows per chunk of the CTA-tiled path: keeps a chunk's inputs and edge weights
 // at ~64 registers (sgwls_tile.cuh).
+#ifndef SGWLS_CHUNK_REGS
+#define SGWLS_CHUNK_REGS 64
+#endif
 __host__ __device__ constexpr int tile_rows_per_chunk(int R, int C) {
-    return (64 / ((2 * R + 1) * (C + R))) < 1 ? 1 : ((64 / ((2 * R + 1) * (C + R))) > 8 ? 8 : (64 / ((2 * R + 1) * (C + R))));
+    return (SGWLS_CHUNK_REGS / ((2 * R + 1) * (C + R))) < 1
+               ? 1
+               : ((SGWLS_CHUNK_REGS / ((2 * R + 1) * (C + R))) > 8 ? 8 : (SGWLS_CHUNK_REGS / ((2 * R + 1) * (C + R))));
 }
 constexpr int kTileMaxR = 4;
 constexpr int kTileWarps = 8;

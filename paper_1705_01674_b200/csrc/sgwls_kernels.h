@@ -27,7 +27,10 @@ struct PassLaunch {
     unsigned long long* err;  // NaN-weight report (first pass only), or nullptr
     const WeightDev* w;
     int* counters = nullptr;  // tiled path: per-band-group tile counters (zeroed; self-resetting)
-    float* crec = nullptr;    // tiled path: every chunk's record (KA -> KB), [chunk][field][line]
+    float* crec = nullptr;    // tiled path: every chunk's record (KA -> KC), [chunk][field][line]
+    float* sep = nullptr;     // tiled path: every chunk separator (KC -> KB), [chunk][q][c][line]
+    int nwa = 8;              // tiled path: chunks per KA tile (super-chunk); == nw unless kc
+    int kc = 0;               // tiled path: separate KC launch for the chunk separators
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);

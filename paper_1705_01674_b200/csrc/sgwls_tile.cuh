@@ -50,6 +50,20 @@ namespace tile {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Bulk (TMA) shared -> global copy; 16-byte aligned addresses, size % 16 == 0.
+__device__ __forceinline__ void bulk_s2g(float* gdst, const float* ssrc, unsigned bytes) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(ssrc);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(sa), "r"(bytes)
+                 : "memory");
+}
+// shared memory must stay valid until the bulk copies have read it
+__device__ __forceinline__ void bulk_commit_and_wait_read() {
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// order this thread's generic-proxy shared-memory writes before async-proxy reads
+__device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("SGWLS_PDL");  // tuning knob: 0 = ordinary stream-ordered launches
@@ -866,8 +880,9 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
 struct TileOut {
     float* out;
     int transpose_out;
-    int step;  // CTA band stride (32 - halo)
-    int nph;   // accumulation phases
+    int step;       // CTA band stride (32 - halo)
+    int nph;        // accumulation phases
+    int early_rec;  // INNER: the predecessor is a separate K2 launch (records complete before it triggers)
 };
 
 __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, int& bmax) {
@@ -884,14 +899,71 @@ __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, in
     }
 }
 
-template <int R, int C, int CG>
+// ===================================================================== KC
+//
+// Every chunk separator from the super-separators: thread (tile J, line L)
+// solves the tile's inner separators with the two known super-separators as
+// boundary values from KA's chunk records (lane per line, fully parallel over
+// tiles), and writes all separators of the tile's chunks to `sep`
+// ([chunk][q][c][line]).  KB then solves every chunk interior independently.
+template <int R, int C>
+__global__ void __launch_bounds__(256) kc_inner(const PassGeom g, int NWA, const float* __restrict__ crec,
+                                                const float* __restrict__ zs, float* __restrict__ sep) {
+    using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, ty = threadIdx.y, NTY = blockDim.y;
+    const int tid = ty * 32 + lane, NT = NTY * 32;
+    const int NL = g.nb * g.batch;
+    const long long NLl = NL;
+    const int L = blockIdx.x * 32 + lane;
+    const int J = blockIdx.y * NTY + ty;
+    const int PSA = (g.P + NWA - 1) / NWA;
+    pdl_wait();  // K2's super-separators (and, through K2, KA's records)
+    pdl_trigger();
+    if (L >= NL || J >= PSA) return;
+    const int nw = min(NWA, g.P - J * NWA);
+    const bool has_l = J > 0, has_r = J < PSA - 1;
+    float zL[R][C], zR[R][C];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            zL[q][c] = has_l ? zs[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
+            zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
+        }
+    float* out = sep + (long long)J * NWA * R * C * NLl + L;
+    if (has_r) {  // the tile's last separator is the super-separator (stored before the solve, see KB note)
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) out[((long long)((nw - 1) * R + q) * C + c) * NLl] = zR[q][c];
+    }
+    solve_inner<R, C>(crec + (long long)J * NWA * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, nw, has_l, zL,
+                      has_r, zR, out, NLl, sm + tid, NT);
+}
+
+template <int R, int C>
+__host__ inline size_t kc_smem(int NWA, int nty) {
+    using RL = Rec<R, C>;
+    return (size_t)(NWA > 1 ? NWA - 1 : 1) * R * RL::RS * 32 * nty * sizeof(float);
+}
+
+// ===================================================================== KB
+
+// Two ways to get a chunk's separators:
+//   INNER = false: from `zsep` = every chunk separator, written by KC;
+//   INNER = true : KB tiles coincide with KA tiles; the tile loads its chunk
+//                  records (`crec`) into shared memory and warp 0 solves the
+//                  inner separators from the two super-separators `zsep` = zs
+//                  (one launch fewer per pass: better for small images).
+template <int R, int C, int CG, bool INNER>
 __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restrict__ src,
-                                               const float* __restrict__ guid, const float* __restrict__ zs,
+                                               const float* __restrict__ guid, const float* __restrict__ zsep,
                                                const float* __restrict__ crec, const TileOut to,
                                                unsigned long long* __restrict__ err,
                                                const __grid_constant__ WeightDev W) {
     constexpr int RW = rows_per_chunk(R, C);
-    constexpr int M = 2 * R + 1, K = RW * M, NF = R + C;
+    constexpr int M = 2 * R + 1, K = RW * M;
     using RL = Rec<R, C>;
     extern __shared__ float sm[];
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
@@ -902,7 +974,6 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int img = blockIdx.z;
     const int j = J * NW + wid;
     const int nw = min(NW, g.P - J * NW);
-    const int PS = (g.P + NW - 1) / NW;
     const bool active = (b < g.nb) && (wid < nw);
     const int L = img * g.nb + b;
     const long long NLl = (long long)g.nb * g.batch;
@@ -910,73 +981,42 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int Y0 = J * NW * RW;
     const int TR = min(NW * RW, g.Hl - Y0);  // tile rows
 
-    // smem carve: [recs | zint | bsc] overlaid by [state]; then [tile]
+    // smem: INNER: [recs | zint | bsc] then the output tile; else the tile only
     const int rs = NT + 1;
     float* recs = sm;                                    // REC x rs
     float* zint = recs + RL::REC * rs;                   // NW x R*C x 32
     float* bsc = zint + NW * R * C * 32;                 // (NW) x R x RS x 32 back-substitution rows
-    const int region1 = (RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32 + 3) & ~3;
-    float* tl = sm + region1;                            // output tile
+    const int region1 = INNER ? (RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32 + 3) & ~3 : 0;
+    float* tl = sm + region1;                            // output tile [x][y*C + c]
     const int bl = min(B0 + 32, g.nb) - 1;
     const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
     const int ncol = xb - xa + 1;
     const int TP = ((TR * C + 3) & ~3) + 4;              // tile pitch (per x line), 16-byte rows
 
-    // ---- 1. spike-forward of every chunk (records to smem)
+    // ---- 1. chunk inputs and edge weights, before the wait when separators
+    //         come from a predecessor (KA finished with the pass input before
+    //         K2/KC trigger); single-chunk lines wait first.
     ChunkIn<R, C, CG, RW> in;
     const int y0 = j * RW;
     const int nrows = active ? min(RW, g.Hl - y0) : 0;
     const int lo = active ? band_lo(g, b) : 0;
-    // With chunk records (KA + K2 ran) everything up to the separators is
-    // already complete when this grid may launch (K2 triggers after its own
-    // wait); without them the pass input comes straight from the predecessor.
-    if (crec == nullptr) pdl_wait();
-    if (active) {
+    // KA's records may be read before the wait only when the predecessor is a
+    // K2/KC launch (those trigger after waiting for KA); after a fused or
+    // absent K2 the predecessor is KA itself.
+    const bool multi = g.P > 1;
+    const bool early = multi && (!INNER || to.early_rec);
+    if (!early) pdl_wait();
+    if (active)
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
                                  L);
-        if (crec != nullptr) {  // KA's record of this chunk
-            const float* srcr = crec + (long long)j * RL::REC * NLl + L;
+    if (INNER && multi && active) {  // KA's record of this chunk
+        const float* srcr = crec + (long long)j * RL::REC * NLl + L;
 #pragma unroll
-            for (int f = 0; f < RL::REC; ++f) recs[f * rs + tid] = srcr[(long long)f * NLl];
-        } else {
-            chunk_spike_forward<R, C, CG, RW>(in, lam, j > 0, j == g.P - 1, nrows * M, recs + tid, rs);
-        }
+        for (int f = 0; f < RL::REC; ++f) recs[f * rs + tid] = srcr[(long long)f * NLl];
     }
-    if (crec != nullptr) pdl_wait();  // K2's separators
+    if (early) pdl_wait();  // separators
     pdl_trigger();
-    __syncthreads();
 
-    // ---- 2. lane-per-band solve of the tile's inner separators with the two
-    //         known super-separators as boundary values
-    if (wid == 0 && b < g.nb) {
-        const bool has_l = J > 0, has_r = J < PS - 1;
-        float zL[R][C], zR[R][C];
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-#pragma unroll
-            for (int c = 0; c < C; ++c) {
-                zL[q][c] = has_l ? zs[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
-                zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
-            }
-        // The boundary values are stored BEFORE the solve: nvcc 12.9 was seen to
-        // reuse the register holding `nw` as the back-substitution loop counter
-        // and then address `zint[nw - 1]` with the decremented value.
-        if (has_r) {
-#pragma unroll
-            for (int q = 0; q < R; ++q)
-#pragma unroll
-                for (int c = 0; c < C; ++c) zint[(((nw - 1) * R + q) * C + c) * 32 + lane] = zR[q][c];
-        }
-        // publish the left super-separator for the tile's first chunk (slot after the bs rows)
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-#pragma unroll
-            for (int c = 0; c < C; ++c) bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane] = zL[q][c];
-        solve_inner<R, C>(recs + lane, rs, 32, nw, has_l, zL, has_r, zR, zint + lane, 32, bsc + lane, 32);
-    }
-    __syncthreads();
-
-    // ---- 3. every chunk: interior solve with known separators
     float zl[R][C], zr[R][C];
 #pragma unroll
     for (int q = 0; q < R; ++q)
@@ -986,26 +1026,72 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             zr[q][c] = 0.f;
         }
     const bool lastc = (j == g.P - 1);
-    if (active) {
+    if constexpr (INNER) {
+        const int PS = (g.P + NW - 1) / NW;
+        __syncthreads();
+        // ---- 2. lane-per-band solve of the tile's inner separators with the
+        //         two known super-separators as boundary values
+        if (wid == 0 && b < g.nb && multi) {
+            const bool has_l = J > 0, has_r = J < PS - 1;
+            float zL[R][C], zR[R][C];
 #pragma unroll
-        for (int q = 0; q < R; ++q)
+            for (int q = 0; q < R; ++q)
 #pragma unroll
-            for (int c = 0; c < C; ++c) {
-                if (j > 0)
-                    zl[q][c] = (wid == 0) ? bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane]
-                                          : zint[(((wid - 1) * R + q) * C + c) * 32 + lane];
-                if (!lastc) zr[q][c] = zint[((wid * R + q) * C + c) * 32 + lane];
+                for (int c = 0; c < C; ++c) {
+                    zL[q][c] = has_l ? zsep[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
+                    zR[q][c] = has_r ? zsep[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
+                }
+            // The boundary values are stored BEFORE the solve: nvcc 12.9 was seen to
+            // reuse the register holding `nw` as the back-substitution loop counter
+            // and then address `zint[nw - 1]` with the decremented value.
+            if (has_r) {
+#pragma unroll
+                for (int q = 0; q < R; ++q)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) zint[(((nw - 1) * R + q) * C + c) * 32 + lane] = zR[q][c];
             }
+            // publish the left super-separator for the tile's first chunk (slot after the bs rows)
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane] = zL[q][c];
+            solve_inner<R, C>(recs + lane, rs, 32, nw, has_l, zL, has_r, zR, zint + lane, 32, bsc + lane, 32);
+        }
+        __syncthreads();
+        if (active && multi) {
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    if (j > 0)
+                        zl[q][c] = (wid == 0) ? bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane]
+                                              : zint[(((wid - 1) * R + q) * C + c) * 32 + lane];
+                    if (!lastc) zr[q][c] = zint[((wid * R + q) * C + c) * 32 + lane];
+                }
+        }
+    } else {
+        // ---- 2. this chunk's two separators (KC)
+        if (active && multi) {
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) {
+                    if (j > 0) zl[q][c] = zsep[((long long)(j - 1) * R * C + q * C + c) * NLl + L];
+                    if (!lastc) zr[q][c] = zsep[((long long)j * R * C + q * C + c) * NLl + L];
+                }
+        }
     }
     const int kv = nrows * M;
     const int kend = lastc ? kv : kv - R;  // interior positions [0, kend)
-    // per-column output scale (1/count if this CTA owns the column, else 0)
+    // per-column averaging scale 1/count, positive if this CTA owns the column
+    // (writes it out), negative otherwise
     float* inv_col = tl + ncol * TP;
     for (int xl = tid; xl < ncol; xl += NT) {
         int bmin, bmax;
         covering(g, xa + xl, bmin, bmax);
         const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
-        inv_col[xl] = own == (int)blockIdx.x ? 1.0f / (float)(bmax - bmin + 1) : 0.f;
+        const float inv = 1.0f / (float)(bmax - bmin + 1);
+        inv_col[xl] = own == (int)blockIdx.x ? inv : -inv;
     }
     if (to.nph > 1)
         for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -1028,8 +1114,12 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     __syncthreads();
     // ---- 4. averaging into the shared output tile, fixed phase order
     //         (nph == 1: no two bands overlap, every tile cell has one writer)
+    //         Values enter the tile already divided by their column's count.
     const int par0 = y0 & 1;
     float* tbase = tl + (lo - xa) * TP + (y0 - Y0) * C;
+    float csc[M];
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj) csc[jj] = active ? fabsf(inv_col[lo - xa + jj]) : 0.f;
     for (int ph = 0; ph < to.nph; ++ph) {
         if (active && (lane % to.nph) == ph) {
 #pragma unroll
@@ -1037,55 +1127,60 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                 if (p < kv) {
                     const int rr = p / M, jj = p % M;
                     const int oe = jj * TP + rr * C, oo = (M - 1 - jj) * TP + rr * C;
-                    float* tp = tbase + (((par0 ^ (rr & 1)) != 0) ? oo : oe);
+                    const bool rev = (par0 ^ (rr & 1)) != 0;
+                    float* tp = tbase + (rev ? oo : oe);
+                    const float sc = rev ? csc[M - 1 - jj] : csc[jj];
                     if (to.nph == 1) {
 #pragma unroll
-                        for (int c = 0; c < C; ++c) tp[c] = ys[p][c];
+                        for (int c = 0; c < C; ++c) tp[c] = ys[p][c] * sc;
                     } else {
 #pragma unroll
-                        for (int c = 0; c < C; ++c) tp[c] += ys[p][c];
+                        for (int c = 0; c < C; ++c) tp[c] = fmaf(ys[p][c], sc, tp[c]);
                     }
                 }
             }
         }
+        fence_proxy_async_shared();  // the tile is read by bulk copies (async proxy) below
         __syncthreads();
     }
-    // ---- 5. owned columns -> global, coalesced.  A warp writes `per` whole
-    //         output columns (transposed layout: TR*C contiguous floats each)
-    //         per step, lanes split as (column, float4) -- no per-element division.
+    // ---- 5. owned columns -> global.  Transposed layout: each owned column is
+    //         TR*C contiguous floats of the output, moved by one bulk (TMA)
+    //         shared->global copy issued by one thread; no register traffic.
     float* oi = to.out + img * g.img_stride;
     if (to.transpose_out) {
         const int n = TR * C;
         const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
                          ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
-        const int nv = vec ? (n >> 2) : n;  // vectors per output column
-        // Thread tid owns vector slot e of columns c0, c0 + cps, ...: one
-        // division per thread, then pointer increments.
-        const int cps = nv <= NT ? NT / nv : 1;  // columns per CTA step
-        const int c0 = nv <= NT ? tid / nv : 0;
-        const int e = tid - c0 * nv;
-        if (c0 < cps && e < nv) {
-            const long long ostep = (long long)cps * g.Hl * C;
-            float* op = oi + ((long long)(xa + c0) * g.Hl + Y0) * C;
-            const float* tp = tl + c0 * TP;
-            if (vec) {
-                for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
-                    const float sc = inv_col[xl];
-                    if (sc == 0.f) continue;
-                    for (int e4 = e; e4 < nv; e4 += NT) {
-                        float4 v = reinterpret_cast<const float4*>(tp)[e4];
-                        v.x *= sc;
-                        v.y *= sc;
-                        v.z *= sc;
-                        v.w *= sc;
-                        reinterpret_cast<float4*>(op)[e4] = v;
-                    }
+        if (vec && n >= 64) {  // >= 256-byte runs: one bulk copy per owned column
+            bool issued = false;
+            for (int xl = tid; xl < ncol; xl += NT) {
+                if (inv_col[xl] > 0.f) {
+                    bulk_s2g(oi + ((long long)(xa + xl) * g.Hl + Y0) * C, tl + xl * TP, (unsigned)(n * 4));
+                    issued = true;
                 }
-            } else {
-                for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
-                    const float sc = inv_col[xl];
-                    if (sc == 0.f) continue;
-                    for (int e2 = e; e2 < nv; e2 += NT) op[e2] = tp[e2] * sc;
+            }
+            if (issued) bulk_commit_and_wait_read();
+        } else {
+            // short runs: thread tid owns vector slot e of columns c0, c0 + cps, ...
+            const int nv = vec ? (n >> 2) : n;
+            const int cps = nv <= NT ? NT / nv : 1;
+            const int c0 = nv <= NT ? tid / nv : 0;
+            const int e = tid - c0 * nv;
+            if (c0 < cps && e < nv) {
+                const long long ostep = (long long)cps * g.Hl * C;
+                float* op = oi + ((long long)(xa + c0) * g.Hl + Y0) * C;
+                const float* tp = tl + c0 * TP;
+                if (vec) {
+                    for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
+                        if (inv_col[xl] <= 0.f) continue;
+                        for (int e4 = e; e4 < nv; e4 += NT)
+                            reinterpret_cast<float4*>(op)[e4] = reinterpret_cast<const float4*>(tp)[e4];
+                    }
+                } else {
+                    for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
+                        if (inv_col[xl] <= 0.f) continue;
+                        for (int e2 = e; e2 < nv; e2 += NT) op[e2] = tp[e2];
+                    }
                 }
             }
         }
@@ -1094,8 +1189,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             float* orow = oi + ((long long)(Y0 + yl) * g.Wl + xa) * C;
             for (int e2 = lane; e2 < ncol * C; e2 += 32) {
                 const int xl = e2 / C, c = e2 - xl * C;
-                const float sc = inv_col[xl];
-                if (sc != 0.f) orow[e2] = tl[xl * TP + yl * C + c] * sc;
+                if (inv_col[xl] > 0.f) orow[e2] = tl[xl * TP + yl * C + c];
             }
         }
     }
@@ -1104,15 +1198,12 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
 // =========================================================== host helpers
 
 template <int R, int C>
-__host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
-    constexpr int RW = rows_per_chunk(R, C);
-    constexpr int K = RW * (2 * R + 1), NF = R + C;
+__host__ inline size_t kb_smem_bytes(bool inner, int NW, int TR, int ncol) {
     using RL = Rec<R, C>;
-    const int NT = NW * 32;
-    const size_t r1a = (size_t)RL::REC * (NT + 1) + (size_t)NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32;
-    const size_t r1 = (r1a + 3) & ~(size_t)3;
-    (void)K;
-    (void)NF;
+    const size_t NT = (size_t)NW * 32;
+    const size_t r1 = inner ? (((size_t)RL::REC * (NT + 1) + NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32 + 3) &
+                               ~(size_t)3)
+                            : 0;
     return (r1 + (size_t)ncol * (((TR * C + 3) & ~3) + 4) + ncol) * sizeof(float);
 }
 
@@ -1124,27 +1215,30 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
     using RL = Rec<R, C>;
     const PassGeom& g = pl.geom;
     const int NL = g.nb * g.batch;
-    const int NW = pl.nw;
-    const int PS = (g.P + NW - 1) / NW;
+    const bool kc = pl.kc != 0;            // separators from KC (else KB solves its tile's inner ones)
+    const int NWA = kc ? pl.nwa : pl.nw;   // KA super-chunk (chunks per KA tile)
+    const int NW = pl.nw;                  // KB tile height (chunks)
+    const int PSA = (g.P + NWA - 1) / NWA;
+    const int PB = (g.P + NW - 1) / NW;
     cudaError_t e;
-    if (PS > 1) {
-        const bool fuse = tile_fuse_k2(PS) && pl.counters != nullptr;
+    if (g.P > 1) {
+        const bool fuse = tile_fuse_k2(PSA) && pl.counters != nullptr;
         {
             ProfScope ps("ka_tile", st);
-            const size_t smem_ka = (size_t)RL::REC * (NW * 32 + 1) * sizeof(float);
-            const size_t smem_k2 = fuse ? k2_tree_smem<R, C>(NW) : 0;
+            const size_t smem_ka = (size_t)RL::REC * (NWA * 32 + 1) * sizeof(float);
+            const size_t smem_k2 = fuse ? k2_tree_smem<R, C>(NWA) : 0;
             const size_t smem = smem_ka > smem_k2 ? smem_ka : smem_k2;
             e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PS), dim3(32, NW), smem, st, g, pl.src, pl.guid,
-                           pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w);
+            e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, NWA), smem, st, g, pl.src,
+                           pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w);
             if (e != cudaSuccess) return e;
         }
-        if (!fuse) {
+        if (PSA > 1 && !fuse) {
             ProfScope ps("k2_tree", st);
             PassGeom gs = g;
-            gs.P = PS;
-            const int NG = PS >= 64 ? 16 : 8;
+            gs.P = PSA;
+            const int NG = PSA >= 64 ? 16 : 8;
             const size_t sm2 = k2_tree_smem<R, C>(NG);
             e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
             if (e != cudaSuccess) return e;
@@ -1152,17 +1246,35 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
                            pl.z);
             if (e != cudaSuccess) return e;
         }
+        if (kc) {
+            ProfScope ps("kc_inner", st);
+            const int nty = 4;
+            const size_t smc = kc_smem<R, C>(NWA, nty);
+            e = cudaFuncSetAttribute(kc_inner<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
+            if (e != cudaSuccess) return e;
+            e = launch_pdl(kc_inner<R, C>, dim3((NL + 31) / 32, (PSA + nty - 1) / nty), dim3(32, nty), smc, st, g, NWA,
+                           (const float*)pl.crec, (const float*)pl.z, pl.sep);
+            if (e != cudaSuccess) return e;
+        }
     }
     {
         ProfScope ps("kb_tile", st);
         constexpr int RW = rows_per_chunk(R, C);
         const int ncol = 31 * g.tau + 2 * g.r + 1;
-        const size_t smem = kb_smem_bytes<R, C>(NW, NW * RW, ncol);
-        e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph};
-        e = launch_pdl(kb_tile<R, C, CG>, dim3(pl.ncta, PS, g.batch), dim3(32, NW), smem, st, g, pl.src, pl.guid,
-                       (const float*)pl.z, (const float*)(PS > 1 ? pl.crec : nullptr), to, pl.err, *pl.w);
+        const size_t smem = kb_smem_bytes<R, C>(!kc, NW, NW * RW, ncol);
+        const bool k2_separate = g.P > 1 && PSA > 1 && !(tile_fuse_k2(PSA) && pl.counters != nullptr);
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, k2_separate ? 1 : 0};
+        if (kc) {
+            e = cudaFuncSetAttribute(kb_tile<R, C, CG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            e = launch_pdl(kb_tile<R, C, CG, false>, dim3(pl.ncta, PB, g.batch), dim3(32, NW), smem, st, g, pl.src,
+                           pl.guid, (const float*)pl.sep, (const float*)nullptr, to, pl.err, *pl.w);
+        } else {
+            e = cudaFuncSetAttribute(kb_tile<R, C, CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            e = launch_pdl(kb_tile<R, C, CG, true>, dim3(pl.ncta, PB, g.batch), dim3(32, NW), smem, st, g, pl.src,
+                           pl.guid, (const float*)pl.z, (const float*)pl.crec, to, pl.err, *pl.w);
+        }
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();

@@ -135,4 +135,4 @@ def test_chunking_invariants(extent, sweep, r, tau):
 def test_kernel_launch_accounting():
     cfg = S.SmoothConfig(lambda_=400.0, r=1, tau=3, iterations=4)
     n = S.kernel_launches(1920, 1080, 3, 1, 1, False, cfg)
-    assert n == 1 + 4 * 3  # guidance transpose + 4 passes x (KA, K2 tree, KB)
+    assert n == 1 + 4 * 3  # guidance transpose + 4 passes x (KA, K2 tree, KB); r = 1 solves inner separators in KB
