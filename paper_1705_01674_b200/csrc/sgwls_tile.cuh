@@ -991,7 +991,22 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int bl = min(B0 + 32, g.nb) - 1;
     const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
     const int ncol = xb - xa + 1;
-    const int TP = ((TR * C + 3) & ~3) + 4;              // tile pitch (per x line), 16-byte rows
+    // Output tile layout.  Column-major [x][y*C + c] (pitch TP, 16-byte rows)
+    // when every owned column leaves as one bulk copy; otherwise row-major
+    // [y][x*C + c] with an odd pitch XP, so that the 32 bands of a warp
+    // (columns tau apart) hit distinct banks when they accumulate.
+    float* oi = to.out + img * g.img_stride;
+    const int n = TR * C;
+    const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
+    // Column-major accumulation is 4-way bank-conflicted for odd tau (pitch = 4
+    // mod 8) and 8-way for even tau: even tau with one channel goes row-major
+    // (2-way) unless bulk copies apply.
+    const bool colmaj = to.transpose_out && vec && (n >= 64 || (g.tau & 1) || C > 1);
+    const int TP = ((n + 3) & ~3) + ((((n + 3) & ~3) % 8 == 0) ? 4 : 8);
+    const int XP = (ncol * C) | 1;
+    const int sx = colmaj ? TP : C, sy = colmaj ? C : XP;  // tile strides of x and y
+    const int tsize = colmaj ? ncol * TP : TR * XP;
 
     // ---- 1. chunk inputs and edge weights, before the wait when separators
     //         come from a predecessor (KA finished with the pass input before
@@ -1085,7 +1100,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int kend = lastc ? kv : kv - R;  // interior positions [0, kend)
     // per-column averaging scale 1/count, positive if this CTA owns the column
     // (writes it out), negative otherwise
-    float* inv_col = tl + ncol * TP;
+    float* inv_col = tl + ((tsize + 3) & ~3);
     for (int xl = tid; xl < ncol; xl += NT) {
         int bmin, bmax;
         covering(g, xa + xl, bmin, bmax);
@@ -1093,8 +1108,12 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         const float inv = 1.0f / (float)(bmax - bmin + 1);
         inv_col[xl] = own == (int)blockIdx.x ? inv : -inv;
     }
-    if (to.nph > 1)
-        for (int i = tid; i < (ncol * TP) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (to.nph > 1) {
+        if (colmaj)
+            for (int i = tid; i < tsize / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        else
+            for (int i = tid; i < tsize; i += NT) tl[i] = 0.f;
+    }
 
     // chunk factor state in registers: couplings cs[p][i] and y / u values ys[p][c]
     float cs[K][R], ys[K][C];
@@ -1116,7 +1135,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     //         (nph == 1: no two bands overlap, every tile cell has one writer)
     //         Values enter the tile already divided by their column's count.
     const int par0 = y0 & 1;
-    float* tbase = tl + (lo - xa) * TP + (y0 - Y0) * C;
+    float* tbase = tl + (lo - xa) * sx + (y0 - Y0) * sy;
     float csc[M];
 #pragma unroll
     for (int jj = 0; jj < M; ++jj) csc[jj] = active ? fabsf(inv_col[lo - xa + jj]) : 0.f;
@@ -1126,7 +1145,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             for (int p = 0; p < K; ++p) {
                 if (p < kv) {
                     const int rr = p / M, jj = p % M;
-                    const int oe = jj * TP + rr * C, oo = (M - 1 - jj) * TP + rr * C;
+                    const int oe = jj * sx + rr * sy, oo = (M - 1 - jj) * sx + rr * sy;
                     const bool rev = (par0 ^ (rr & 1)) != 0;
                     float* tp = tbase + (rev ? oo : oe);
                     const float sc = rev ? csc[M - 1 - jj] : csc[jj];
@@ -1144,52 +1163,50 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         __syncthreads();
     }
     // ---- 5. owned columns -> global.  Transposed layout: each owned column is
-    //         TR*C contiguous floats of the output, moved by one bulk (TMA)
-    //         shared->global copy issued by one thread; no register traffic.
-    float* oi = to.out + img * g.img_stride;
-    if (to.transpose_out) {
-        const int n = TR * C;
-        const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
-                         ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
-        if (vec && n >= 64) {  // >= 256-byte runs: one bulk copy per owned column
-            bool issued = false;
-            for (int xl = tid; xl < ncol; xl += NT) {
-                if (inv_col[xl] > 0.f) {
-                    bulk_s2g(oi + ((long long)(xa + xl) * g.Hl + Y0) * C, tl + xl * TP, (unsigned)(n * 4));
-                    issued = true;
-                }
+    //         TR*C contiguous floats of the output.
+    if (colmaj && n >= 64) {  // >= 256-byte runs: one bulk (TMA) shared->global copy per owned column
+        bool issued = false;
+        for (int xl = tid; xl < ncol; xl += NT) {
+            if (inv_col[xl] > 0.f) {
+                bulk_s2g(oi + ((long long)(xa + xl) * g.Hl + Y0) * C, tl + xl * TP, (unsigned)(n * 4));
+                issued = true;
             }
-            if (issued) bulk_commit_and_wait_read();
-        } else {
-            // short runs: thread tid owns vector slot e of columns c0, c0 + cps, ...
-            const int nv = vec ? (n >> 2) : n;
-            const int cps = nv <= NT ? NT / nv : 1;
-            const int c0 = nv <= NT ? tid / nv : 0;
-            const int e = tid - c0 * nv;
-            if (c0 < cps && e < nv) {
-                const long long ostep = (long long)cps * g.Hl * C;
-                float* op = oi + ((long long)(xa + c0) * g.Hl + Y0) * C;
-                const float* tp = tl + c0 * TP;
-                if (vec) {
-                    for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
-                        if (inv_col[xl] <= 0.f) continue;
-                        for (int e4 = e; e4 < nv; e4 += NT)
-                            reinterpret_cast<float4*>(op)[e4] = reinterpret_cast<const float4*>(tp)[e4];
-                    }
-                } else {
-                    for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
-                        if (inv_col[xl] <= 0.f) continue;
-                        for (int e2 = e; e2 < nv; e2 += NT) op[e2] = tp[e2];
-                    }
-                }
+        }
+        if (issued) bulk_commit_and_wait_read();
+    } else if (colmaj) {  // short runs, column-major tile: float4 slot e4 of columns c0, c0 + cps, ...
+        const int nv = n >> 2;
+        const int cps = nv <= NT ? NT / nv : 1;
+        const int c0 = nv <= NT ? tid / nv : 0;
+        const int e = tid - c0 * nv;
+        if (c0 < cps && e < nv) {
+            const long long ostep = (long long)cps * g.Hl * C;
+            float* op = oi + ((long long)(xa + c0) * g.Hl + Y0) * C;
+            const float* tp = tl + c0 * TP;
+            for (int xl = c0; xl < ncol; xl += cps, op += ostep, tp += cps * TP) {
+                if (inv_col[xl] <= 0.f) continue;
+                for (int e4 = e; e4 < nv; e4 += NT)
+                    reinterpret_cast<float4*>(op)[e4] = reinterpret_cast<const float4*>(tp)[e4];
+            }
+        }
+    } else if (to.transpose_out) {
+        // thread tid owns element e of columns c0, c0 + cps, ... (row-major tile)
+        const int cps = n <= NT ? NT / n : 1;
+        const int c0 = n <= NT ? tid / n : 0;
+        const int e = tid - c0 * n;
+        if (c0 < cps && e < n) {
+            const long long ostep = (long long)cps * g.Hl * C;
+            float* op = oi + ((long long)(xa + c0) * g.Hl + Y0) * C;
+            for (int xl = c0; xl < ncol; xl += cps, op += ostep) {
+                if (inv_col[xl] <= 0.f) continue;
+                for (int e2 = e; e2 < n; e2 += NT) op[e2] = tl[(e2 / C) * XP + xl * C + e2 % C];
             }
         }
     } else {
         for (int yl = wid; yl < TR; yl += NW) {
             float* orow = oi + ((long long)(Y0 + yl) * g.Wl + xa) * C;
             for (int e2 = lane; e2 < ncol * C; e2 += 32) {
-                const int xl = e2 / C, c = e2 - xl * C;
-                if (inv_col[xl] > 0.f) orow[e2] = tl[xl * TP + yl * C + c];
+                const int xl = e2 / C;
+                if (inv_col[xl] > 0.f) orow[e2] = tl[yl * XP + e2];
             }
         }
     }
@@ -1204,7 +1221,8 @@ __host__ inline size_t kb_smem_bytes(bool inner, int NW, int TR, int ncol) {
     const size_t r1 = inner ? (((size_t)RL::REC * (NT + 1) + NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32 + 3) &
                                ~(size_t)3)
                             : 0;
-    return (r1 + (size_t)ncol * (((TR * C + 3) & ~3) + 4) + ncol) * sizeof(float);
+    const int n4 = (TR * C + 3) & ~3;
+    return (r1 + (size_t)ncol * (n4 + (n4 % 8 == 0 ? 4 : 8)) + ncol) * sizeof(float);
 }
 
 
