@@ -188,8 +188,8 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         const int n = v ? std::atoi(v) : 0;
         return n < 0 ? 0 : (n > 8 ? 8 : n);
     }();
-    // measured on B200: 8-chunk tiles for r = 1, 4-chunk tiles for r >= 2
-    const int tile_warps = tile_warps_env ? tile_warps_env : (r == 1 ? kTileWarps : kTileWarps / 2);
+    // measured on B200: 8-chunk KB tiles for r = 1 with several channels, 4-chunk tiles otherwise
+    const int tile_warps = tile_warps_env ? tile_warps_env : ((r == 1 && C >= 2) ? kTileWarps : kTileWarps / 2);
     ap.fast = (!force_generic && !g.degenerate && r <= kTileMaxR && (Cg == 1 || Cg == 3)) ? 1 : 0;
     ap.step = 32;
     ap.ncta = 1;

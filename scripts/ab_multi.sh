@@ -1,0 +1,9 @@
+#!/bin/bash
+# A/B several env combinations: COMBOS="A=1,B=2 A=0" CONFIGS="c2"
+mkdir -p gpurun_out
+for c in ${CONFIGS:-c2}; do for combo in ${COMBOS}; do
+envs=$(echo $combo | tr ',' ' ')
+env $envs timeout 300 python bench.py --config $c --steps ${STEPS:-50} --warmup 3 --no-cpu-baseline --no-e2e --no-prof > gpurun_out/abm.json 2>gpurun_out/abm.err
+python -c "
+import json; d=json.load(open('gpurun_out/abm.json')); print('$c', '$combo', 'MPix/s=%.0f'%d['value'], 'ms=%.4f'%d['ms_per_step'])" 2>&1 | tail -1
+done; done
