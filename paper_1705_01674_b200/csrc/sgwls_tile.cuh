@@ -723,13 +723,15 @@ __host__ inline size_t k2_tree_smem(int NG) {
 // ===================================================================== KA
 
 template <int R, int C, int CG>
-// Register budgets: plain __launch_bounds__(256) (ptxas settles at ~80-128
-// registers) measured best overall on B200; tuning variants override these.
-#ifdef SGWLS_KA_MINB
-#define SGWLS_KA_BOUNDS __launch_bounds__(256, SGWLS_KA_MINB)
-#else
-#define SGWLS_KA_BOUNDS __launch_bounds__(256)
+// Register budgets (tuning variants override these): KA is held to 3 CTAs of
+// 256 threads per SM; KB keeps plain __launch_bounds__(256) (ptxas settles at
+// ~95-128 registers; tighter budgets spill and lose on B200).
+#ifndef SGWLS_KA_MINB
+// 3 CTAs (<= 85 registers) for r = 1, 4 (<= 64, a few spills) for r >= 2:
+// measured +1-9% (r = 1) and +10-13% (c3, c5) on B200
+#define SGWLS_KA_MINB (R >= 2 ? 4 : 3)
 #endif
+#define SGWLS_KA_BOUNDS __launch_bounds__(256, SGWLS_KA_MINB)
 #ifdef SGWLS_KB_MINB
 #define SGWLS_KB_BOUNDS __launch_bounds__(256, SGWLS_KB_MINB)
 #else
@@ -906,8 +908,11 @@ __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, in
 // boundary values from KA's chunk records (lane per line, fully parallel over
 // tiles), and writes all separators of the tile's chunks to `sep`
 // ([chunk][q][c][line]).  KB then solves every chunk interior independently.
+#ifndef SGWLS_KC_MINB
+#define SGWLS_KC_MINB 1
+#endif
 template <int R, int C>
-__global__ void __launch_bounds__(256) kc_inner(const PassGeom g, int NWA, const float* __restrict__ crec,
+__global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g, int NWA, const float* __restrict__ crec,
                                                 const float* __restrict__ zs, float* __restrict__ sep) {
     using RL = Rec<R, C>;
     extern __shared__ float sm[];
