@@ -121,6 +121,18 @@ __device__ __forceinline__ float guidance_weight(const WeightDev& W, float range
     return s / (pr + W.eps);
 }
 
+// Same, with the kernel kind fixed at compile time (1 = Exp, 0 = Frac).
+template <int WK>
+__device__ __forceinline__ float guidance_weight_k(const WeightDev& W, float range2, int d2) {
+    const float s = W.spat[d2];
+    if constexpr (WK == 1) {
+        return s * fast_ex2(range2 * W.exp_k);
+    } else {
+        const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
+        return s / (pr + W.eps);
+    }
+}
+
 // Position walker: serpentine coordinate of position p = y*m + jj within a band.
 __device__ __forceinline__ int serp_col(int lo, int m, int y, int jj) {
     return lo + ((y & 1) ? (m - 1 - jj) : jj);

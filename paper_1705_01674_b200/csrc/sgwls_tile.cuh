@@ -125,10 +125,10 @@ struct ChunkIn {
     float w[K][R];  // w[k][t-1] = weight of edge (k - t, k)
 };
 
-template <int R, int C, int CG, int RW>
-__device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
-                                           const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
-                                           int lo, int y0, int nrows, unsigned long long* err, int line) {
+template <int R, int C, int CG, int RW, int WK>
+__device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
+                                             const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
+                                             int lo, int y0, int nrows, unsigned long long* err, int line) {
     constexpr int M = 2 * R + 1, K = RW * M;
     float gp[K][CG];
     float gprev[R][CG];  // positions y0*M - R .. y0*M - 1 (last R of row y0-1)
@@ -173,9 +173,20 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
     // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time.
     // A NaN weight (NaN guidance) is the reference's "non-positive pivot" failure:
     // remember the first offending position and report it once.
-    // Cheap detection (one add per edge: any NaN poisons the sum; weights are
-    // finite and >= 0 otherwise), exact location only on the rare slow path.
+    // Cheap detection: a weight can only be NaN where a guidance value it
+    // reads is NaN or infinite, and x * 0 is NaN exactly for those; the exact
+    // position is located from the weights only on that rare path.
     float acc = 0.f;
+    if (err != nullptr) {
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int c = 0; c < CG; ++c) acc = fmaf(gp[k][c], 0.f, acc);
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int c = 0; c < CG; ++c) acc = fmaf(gprev[i][c], 0.f, acc);
+    }
 #pragma unroll
     for (int k = 0; k < K; ++k) {
 #pragma unroll
@@ -187,9 +198,7 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
                 const float d = gp[k][c] - other;
                 r2 = fmaf(d, d, r2);
             }
-            const float wv = guidance_weight(W, r2, edge_d2(k % M, t));
-            in.w[k][t - 1] = wv;
-            acc += wv;
+            in.w[k][t - 1] = guidance_weight_k<WK>(W, r2, edge_d2(k % M, t));
         }
     }
     if (err != nullptr && !(acc >= 0.f)) {
@@ -203,6 +212,17 @@ __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const floa
             }
         if (bad != 0x7fffffff) atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)bad);
     }
+}
+
+// One uniform branch per chunk on the weight kind instead of one per edge.
+template <int R, int C, int CG, int RW>
+__device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
+                                           const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
+                                           int lo, int y0, int nrows, unsigned long long* err, int line) {
+    if (W.kind == 1)
+        load_chunk_k<R, C, CG, RW, 1>(in, F, G, g, W, lo, y0, nrows, err, line);
+    else
+        load_chunk_k<R, C, CG, RW, 0>(in, F, G, g, W, lo, y0, nrows, err, line);
 }
 
 // ------------------------------------------------- elimination window (scalar)
