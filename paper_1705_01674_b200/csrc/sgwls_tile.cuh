@@ -905,6 +905,7 @@ struct TileOut {
     int step;       // CTA band stride (32 - halo)
     int nph;        // accumulation phases
     int early_rec;  // INNER: the predecessor is a separate K2 launch (records complete before it triggers)
+    int rowmaj_odd; // row-major output tile also for odd tau (one channel, short columns)
 };
 
 __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, int& bmax) {
@@ -1025,9 +1026,10 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const bool vec = ((g.Hl * C) % 4 == 0) && ((Y0 * C) % 4 == 0) && (n % 4 == 0) &&
                      ((reinterpret_cast<uintptr_t>(oi) & 15) == 0);
     // Column-major accumulation is 4-way bank-conflicted for odd tau (pitch = 4
-    // mod 8) and 8-way for even tau: even tau with one channel goes row-major
-    // (2-way) unless bulk copies apply.
-    const bool colmaj = to.transpose_out && vec && (n >= 64 || (g.tau & 1) || C > 1);
+    // mod 8) and 8-way for even tau; row-major with an odd pitch is conflict-free
+    // (odd tau) or 2-way (even tau) for one channel, and its columns still leave
+    // as float4 stores (4 gathered rows).  Bulk copies need column-major.
+    const bool colmaj = to.transpose_out && vec && (n >= 64 || C > 1 || ((g.tau & 1) && !to.rowmaj_odd));
     const int TP = ((n + 3) & ~3) + ((((n + 3) & ~3) % 8 == 0) ? 4 : 8);
     const int XP = (ncol * C) | 1;
     const int sx = colmaj ? TP : C, sy = colmaj ? C : XP;  // tile strides of x and y
@@ -1213,6 +1215,23 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                     reinterpret_cast<float4*>(op)[e4] = reinterpret_cast<const float4*>(tp)[e4];
             }
         }
+    } else if (to.transpose_out && vec && C == 1) {
+        // row-major tile, one channel: thread tid gathers 4 rows (slot e4) of
+        // columns c0, c0 + cps, ... into one float4 store
+        const int nv = n >> 2;
+        const int cps = nv <= NT ? NT / nv : 1;
+        const int c0 = nv <= NT ? tid / nv : 0;
+        const int e4 = tid - c0 * nv;
+        if (c0 < cps && e4 < nv) {
+            const long long ostep = (long long)cps * g.Hl;
+            float* op = oi + (long long)(xa + c0) * g.Hl + Y0;
+            const float* tq = tl + 4 * e4 * XP;
+            for (int xl = c0; xl < ncol; xl += cps, op += ostep) {
+                if (inv_col[xl] <= 0.f) continue;
+                reinterpret_cast<float4*>(op)[e4] =
+                    make_float4(tq[xl], tq[XP + xl], tq[2 * XP + xl], tq[3 * XP + xl]);
+            }
+        }
     } else if (to.transpose_out) {
         // thread tid owns element e of columns c0, c0 + cps, ... (row-major tile)
         const int cps = n <= NT ? NT / n : 1;
@@ -1306,7 +1325,11 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         const int ncol = 31 * g.tau + 2 * g.r + 1;
         const size_t smem = kb_smem_bytes<R, C>(!kc, NW, NW * RW, ncol);
         const bool k2_separate = g.P > 1 && PSA > 1 && !(tile_fuse_k2(PSA) && pl.counters != nullptr);
-        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, k2_separate ? 1 : 0};
+        static const int rowmaj_odd = [] {
+            const char* v = std::getenv("SGWLS_ROWMAJ_ODD");  // tuning knob
+            return v ? std::atoi(v) : 1;
+        }();
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, k2_separate ? 1 : 0, rowmaj_odd};
         if (kc) {
             e = cudaFuncSetAttribute(kb_tile<R, C, CG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
