@@ -322,8 +322,14 @@ struct Win {
 // compile to register renames.
 template <int R, int C, int CG, int RW, bool FULL>
 __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                         bool last, int kv, float* rec, int rs) {
+                                                         bool last, int kv, float* rec, int rs, float* grec,
+                                                         long long gs) {
     using RL = Rec<R, C>;
+    // every record field goes to `rec` (shared) and, if given, to `grec` (global)
+    auto put = [&](int f, float v) {
+        rec[f * rs] = v;
+        if (grec != nullptr) grec[f * gs] = v;
+    };
     constexpr int K = RW * (2 * R + 1);
     Win<R, C, true> w;
     w.clear();
@@ -360,31 +366,32 @@ __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG,
 #pragma unroll
         for (int i = 0; i < R; ++i) {
 #pragma unroll
-            for (int k2 = i + 1; k2 < R; ++k2) rec[(RL::TOFF + offi(i, k2, R)) * rs] = w.A[i][k2];
+            for (int k2 = i + 1; k2 < R; ++k2) put(RL::TOFF + offi(i, k2, R), w.A[i][k2]);
 #pragma unroll
-            for (int mm = 0; mm < R; ++mm) rec[(RL::TCROSS + i * R + mm) * rs] = w.Q[i][mm];
-            rec[(RL::TE + i) * rs] = w.e[i];
+            for (int mm = 0; mm < R; ++mm) put(RL::TCROSS + i * R + mm, w.Q[i][mm]);
+            put(RL::TE + i, w.e[i]);
 #pragma unroll
-            for (int c = 0; c < C; ++c) rec[(RL::TG + i * C + c) * rs] = w.g[i][c];
+            for (int c = 0; c < C; ++c) put(RL::TG + i * C + c, w.g[i][c]);
         }
     }
 #pragma unroll
     for (int mm = 0; mm < R; ++mm) {
 #pragma unroll
-        for (int m2 = mm + 1; m2 < R; ++m2) rec[(RL::HOFF + offi(mm, m2, R)) * rs] = w.hoff[mm][m2];
-        rec[(RL::HE + mm) * rs] = w.he[mm];
+        for (int m2 = mm + 1; m2 < R; ++m2) put(RL::HOFF + offi(mm, m2, R), w.hoff[mm][m2]);
+        put(RL::HE + mm, w.he[mm]);
 #pragma unroll
-        for (int c = 0; c < C; ++c) rec[(RL::HG + mm * C + c) * rs] = w.hg[mm][c];
+        for (int c = 0; c < C; ++c) put(RL::HG + mm * C + c, w.hg[mm][c]);
     }
 }
 
 template <int R, int C, int CG, int RW>
 __device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                    bool last, int kv, float* rec, int rs) {
+                                                    bool last, int kv, float* rec, int rs, float* grec = nullptr,
+                                                    long long gs = 0) {
     if (kv == RW * (2 * R + 1))
-        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs);
+        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs, grec, gs);
     else
-        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lam, has_left, last, kv, rec, rs);
+        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lam, has_left, last, kv, rec, rs, grec, gs);
 }
 
 // ---------------------------------------------- block window (separator level)
@@ -784,11 +791,9 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
         ChunkIn<R, C, CG, RW> in;
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows,
                                  nullptr, L);
-        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0, j == g.P - 1, nrows * M, rec, rs);
-        // every chunk record also goes to HBM for KB (saves KB a spike-forward)
-        float* dst = crec + (long long)j * RL::REC * NL + L;
-#pragma unroll
-        for (int f = 0; f < RL::REC; ++f) dst[(long long)f * NL] = rec[f * rs];
+        // every chunk record also goes to HBM for KC / KB (nothing downstream redoes the spike-forward)
+        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0, j == g.P - 1, nrows * M, rec, rs,
+                                          crec + (long long)j * RL::REC * NL + L, (long long)NL);
     }
     __syncthreads();
     const int PS = (g.P + NW - 1) / NW;
@@ -1131,15 +1136,17 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     for (int xl = tid; xl < ncol; xl += NT) {
         int bmin, bmax;
         covering(g, xa + xl, bmin, bmax);
-        const int own = bmax - 31 <= 0 ? 0 : (bmax - 31 + to.step - 1) / to.step;
+        // owner CTA = ceil((bmax - 31) / step) (0 if bmax <= 31), tested without a division
+        const int bx = blockIdx.x, q = bmax - 31;
+        const bool owned = bx == 0 ? q <= 0 : (q > (bx - 1) * to.step && q <= bx * to.step);
         const float inv = 1.0f / (float)(bmax - bmin + 1);
-        inv_col[xl] = own == (int)blockIdx.x ? inv : -inv;
+        inv_col[xl] = owned ? inv : -inv;
     }
     if (to.nph > 1) {
         if (colmaj)
             for (int i = tid; i < tsize / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        else
-            for (int i = tid; i < tsize; i += NT) tl[i] = 0.f;
+        else  // (the tile region is padded to a multiple of 4 floats)
+            for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     // chunk factor state in registers: couplings cs[p][i] and y / u values ys[p][c]
