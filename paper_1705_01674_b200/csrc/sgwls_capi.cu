@@ -137,6 +137,11 @@ void build_weights(const sgwls_b200_config* c, WeightDev& w) {
         else
             s = 1.0 / (std::pow(std::sqrt((double)d2), c->alpha_s) + c->epsilon);
         w.spat[d2] = (float)s;
+        if (d2 < 32) {
+            const double ls = c->lambda * s;
+            w.lspat[d2] = (float)ls;
+            w.lg2ls[d2] = ls > 0.0 ? (float)std::log2(ls) : -INFINITY;
+        }
     }
 }
 
@@ -270,8 +275,23 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
     return ap;
 }
 
+// Ready-flag mode (sgwls_device.cuh kFlagMaxSuper): r = 1 schedule with a
+// short reduced system; the K2 solve runs in KA and KB waits per band group.
+bool flag_mode(const AxisPlan& ap) {
+    static const int env = [] {
+        // tuning knob: 1 = ready-flag mode (measured on B200: c1 -17%, c2 +2% with
+        // SGWLS_KA_JFAST=SGWLS_KB_JFAST=1), so off by default
+        const char* v = std::getenv("SGWLS_FLAGS");
+        return v ? std::atoi(v) : 0;
+    }();
+    if (!env || !ap.fast || ap.kc || ap.g.P <= 1) return false;
+    const int PS = (ap.g.P + ap.nwa - 1) / ap.nwa;
+    return PS > 1 && PS <= kFlagMaxSuper;
+}
+
 int kernels_per_pass(const AxisPlan& ap) {
     if (ap.fast) {  // ka_tile (K2 fused or its own k2_tree), kb_tile
+        if (flag_mode(ap)) return 2;
         const int PS = (ap.g.P + ap.nwa - 1) / ap.nwa;
         static const int fuse_k2 = std::getenv("SGWLS_FUSE_K2") ? std::atoi(std::getenv("SGWLS_FUSE_K2")) : 0;
         // ka_tile [+ k2_tree unless fused] [+ kc_inner] when the lines have several chunks; kb_tile
@@ -353,8 +373,8 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
     crec.alloc(crec_n, st);
     DevBuf sepb;
     sepb.alloc(sep_n, st);
-    cnt.alloc(ngroups, st);
-    CK(cudaMemsetAsync(cnt.p, 0, ngroups * sizeof(float), st));
+    cnt.alloc(2 * ngroups, st);  // [fused-K2 tile counters | ready flags]
+    CK(cudaMemsetAsync(cnt.p, 0, 2 * ngroups * sizeof(float), st));
     rec.alloc(rec_n, st);
     rs.alloc(rs_n, st);
     z.alloc(z_n, st);
@@ -394,7 +414,10 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
             const char* v = std::getenv("SGWLS_FUSE_K2");
             return v ? std::atoi(v) : 0;
         }();
-        pl.counters = fuse_k2 ? reinterpret_cast<int*>(cnt.p) : nullptr;
+        const bool flagged = flag_mode(ap);
+        pl.counters = (fuse_k2 || flagged) ? reinterpret_cast<int*>(cnt.p) : nullptr;
+        pl.flags = flagged ? reinterpret_cast<int*>(cnt.p) + ngroups : nullptr;
+        pl.epoch = p + 1;
         pl.crec = crec.p;
         pl.src = src;
         pl.guid = o == 0 ? d_g : gt.p;

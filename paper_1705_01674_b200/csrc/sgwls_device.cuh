@@ -35,6 +35,9 @@ struct WeightDev {
     float frac_lg2s;   // Frac: log2(gscale^2)
     float eps;         // Frac: epsilon
     float spat[kLutMax];  // spatial factor by squared 2-D distance d2
+    // tiled path (r <= 4, d2 < kTileLut): lambda folded into the weight
+    float lspat[32];      // lambda * spat[d2]                     (Frac)
+    float lg2ls[32];      // log2(lambda * spat[d2]), -inf for 0   (Exp)
 };
 
 // Geometry of one pass in its own (possibly transposed) layout.
@@ -93,6 +96,10 @@ constexpr int kTileWarps = 8;
 // 16-warp tree launch.
 constexpr int kFuseK2MaxSuper = 32;
 __host__ __device__ constexpr bool tile_fuse_k2(int PS) { return PS > 1 && PS <= kFuseK2MaxSuper; }
+// Ready-flag mode (r = 1 schedule KA -> KB): the last KA tile of each band
+// group solves that group's reduced system (depth ~2*PS/NW + NW) and raises a
+// flag; KB tiles wait on their own groups' flags only.
+constexpr int kFlagMaxSuper = 64;
 
 __device__ __forceinline__ float fast_ex2(float x) {
     float y;
@@ -130,6 +137,19 @@ __device__ __forceinline__ float guidance_weight_k(const WeightDev& W, float ran
     } else {
         const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
         return s / (pr + W.eps);
+    }
+}
+
+// lambda * weight for the tiled path (kind fixed at compile time).  Exp:
+// lambda*s*exp2(k*range2) = exp2(k*range2 + log2(lambda*s)): one FFMA + one
+// MUFU per edge instead of FMUL, MUFU and two more FMULs.
+template <int WK>
+__device__ __forceinline__ float guidance_lweight_k(const WeightDev& W, float range2, int d2) {
+    if constexpr (WK == 1) {
+        return fast_ex2(fmaf(range2, W.exp_k, W.lg2ls[d2]));
+    } else {
+        const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
+        return W.lspat[d2] / (pr + W.eps);
     }
 }
 

@@ -31,6 +31,12 @@ struct PassLaunch {
     float* sep = nullptr;     // tiled path: every chunk separator (KC -> KB), [chunk][q][c][line]
     int nwa = 8;              // tiled path: chunks per KA tile (super-chunk); == nw unless kc
     int kc = 0;               // tiled path: separate KC launch for the chunk separators
+    // tiled path, ready-flag mode: KA's last tile per band group solves the
+    // group's reduced system and sets flags[group] = epoch; KB waits until its
+    // groups' flags reach epoch instead of waiting for the whole KA grid.
+    // The flags are zeroed once per call; pass p uses epoch p + 1.
+    int* flags = nullptr;
+    int epoch = 0;
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);

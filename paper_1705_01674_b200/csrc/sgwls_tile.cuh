@@ -64,6 +64,20 @@ __device__ __forceinline__ void bulk_commit_and_wait_read() {
 // order this thread's generic-proxy shared-memory writes before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// gpu-scope release store / acquire load of a ready flag
+__device__ __forceinline__ void st_release_gpu(int* p, int v) {
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// spin until flags[i] reaches epoch (one thread; the caller's barrier publishes it to the CTA)
+__device__ __forceinline__ void wait_flag(const int* flags, int i, int epoch) {
+    while (ld_acquire_gpu(flags + i) < epoch) __nanosleep(64);
+}
+
 inline bool pdl_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("SGWLS_PDL");  // tuning knob: 0 = ordinary stream-ordered launches
@@ -122,7 +136,7 @@ template <int R, int C, int CG, int RW>
 struct ChunkIn {
     static constexpr int M = 2 * R + 1, K = RW * M;
     float f[K][C];
-    float w[K][R];  // w[k][t-1] = weight of edge (k - t, k)
+    float w[K][R];  // w[k][t-1] = lambda * weight of edge (k - t, k)
 };
 
 template <int R, int C, int CG, int RW, int WK>
@@ -198,7 +212,7 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
                 const float d = gp[k][c] - other;
                 r2 = fmaf(d, d, r2);
             }
-            in.w[k][t - 1] = guidance_weight_k<WK>(W, r2, edge_d2(k % M, t));
+            in.w[k][t - 1] = guidance_lweight_k<WK>(W, r2, edge_d2(k % M, t));
         }
     }
     if (err != nullptr && !(acc >= 0.f)) {
@@ -341,7 +355,7 @@ __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG,
             for (int c = 0; c < C; ++c) w.g[R][c] = in.f[k][c];
 #pragma unroll
             for (int t = 1; t <= R; ++t) {
-                const float lw = lam * in.w[k][t - 1];
+                const float lw = in.w[k][t - 1];
                 if (k - t >= 0) {
                     w.A[R - t][R] = lw;
                 } else if (has_left) {
@@ -768,21 +782,29 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
                                                const float* __restrict__ guid, float* __restrict__ srec,
                                                float* __restrict__ rsc, float* __restrict__ zs,
                                                int* __restrict__ counters, float* __restrict__ crec,
-                                               const __grid_constant__ WeightDev W) {
+                                               const __grid_constant__ WeightDev W, int* __restrict__ flags,
+                                               int epoch, int opts) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1;
     using RL = Rec<R, C>;
     extern __shared__ float sm[];
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
     const int NL = g.nb * g.batch;
-    const int L = blockIdx.x * 32 + lane;
-    const int J = blockIdx.y;
+    // grid: (line group, tile) or, with jfast, (tile, line group): the tiles of
+    // one group are then dispatched together and groups complete in order
+    // opts bit 0: jfast grid order; bit 1: trigger the dependent launch only
+    // after this tile's chunks are done (KB's prologue then overlaps the tail
+    // and the reduced solves instead of competing with the chunk work)
+    const bool jfast = opts & 1, late = (opts >> 1) & 1;
+    const int grp = jfast ? blockIdx.y : blockIdx.x;
+    const int L = grp * 32 + lane;
+    const int J = jfast ? blockIdx.x : blockIdx.y;
     const int j = J * NW + wid;
     const int nw = min(NW, g.P - J * NW);
     const int rs = NW * 32 + 1;  // smem record field stride
     float* rec = sm + wid * 32 + lane;
     pdl_wait();  // the pass input is the previous pass's output
-    pdl_trigger();
+    if (!late) pdl_trigger();
     if (L < NL && wid < nw) {
         const int img = L / g.nb, b = L - img * g.nb;
         const int lo = band_lo(g, b);
@@ -796,6 +818,7 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
                                           crec + (long long)j * RL::REC * NL + L, (long long)NL);
     }
     __syncthreads();
+    if (late) pdl_trigger();
     const int PS = (g.P + NW - 1) / NW;
     if (wid == 0 && L < NL) {
         const long long NLl = NL;
@@ -809,16 +832,23 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     __threadfence();  // publish this tile's super-records before counting it
     __syncthreads();
     if (wid == 0 && lane == 0) {
-        const int done = atomicAdd(&counters[blockIdx.x], 1);
+        const int done = atomicAdd(&counters[grp], 1);
         s_last = (done == PS - 1);
-        if (s_last) counters[blockIdx.x] = 0;  // ready for the next pass / replay
+        if (s_last) counters[grp] = 0;  // ready for the next pass / replay
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
     PassGeom gs = g;
     gs.P = PS;
-    k2_tree_body<R, C>(gs, srec, rsc, zs, sm, lane, wid, NW, blockIdx.x);
+    k2_tree_body<R, C>(gs, srec, rsc, zs, sm, lane, wid, NW, grp);
+    if (flags != nullptr) {  // publish: this group's super-separators (and every record) are final
+        __syncthreads();
+        if (wid == 0 && lane == 0) {
+            __threadfence();
+            st_release_gpu(&flags[grp], epoch);
+        }
+    }
 }
 
 // Interior solve of one chunk with both separators known (zl: previous
@@ -860,7 +890,7 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
                 const bool pleft = (k - t < 0);
                 const bool pright = kq && (k - t >= K - R);
                 if (pright) continue;
-                const float lw = lam * in.w[cl(k, K)][t - 1];
+                const float lw = in.w[cl(k, K)][t - 1];
                 if (!kq && !pleft) {
                     w.A[R - t][R] = lw;
                 } else if (!kq && pleft) {
@@ -911,6 +941,9 @@ struct TileOut {
     int nph;        // accumulation phases
     int early_rec;  // INNER: the predecessor is a separate K2 launch (records complete before it triggers)
     int rowmaj_odd; // row-major output tile also for odd tau (one channel, short columns)
+    const int* flags;  // ready-flag mode (INNER): per-band-group flags raised by KA, else nullptr
+    int epoch;         // flag value of this pass
+    int jfast;         // grid order (chunk tile fastest)
 };
 
 __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, int& bmax) {
@@ -999,9 +1032,11 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     extern __shared__ float sm[];
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
     const int tid = wid * 32 + lane, NT = NW * 32;
-    const int B0 = blockIdx.x * to.step;
+    // grid: (band tile, chunk tile, image) or, with jfast, (chunk tile, band tile, image)
+    const int bxi = to.jfast ? blockIdx.y : blockIdx.x;
+    const int B0 = bxi * to.step;
     const int b = B0 + lane;
-    const int J = blockIdx.y;
+    const int J = to.jfast ? blockIdx.x : blockIdx.y;
     const int img = blockIdx.z;
     const int j = J * NW + wid;
     const int nw = min(NW, g.P - J * NW);
@@ -1051,17 +1086,30 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     // K2/KC launch (those trigger after waiting for KA); after a fused or
     // absent K2 the predecessor is KA itself.
     const bool multi = g.P > 1;
-    const bool early = multi && (!INNER || to.early_rec);
+    // ready-flag mode: KA runs the reduced solve per band group and raises a
+    // flag; this tile waits for the (at most two) groups its bands belong to.
+    // Records and separators are then read through L2 (ld.cg: written by a
+    // grid that may still be running).
+    const bool flagged = INNER && multi && to.flags != nullptr;
+    const bool early = flagged || (multi && (!INNER || to.early_rec));
     if (!early) pdl_wait();
     if (active)
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
                                  L);
+    if (flagged) {
+        if (tid == 0) {
+            const int lfirst = img * g.nb + B0, llast = img * g.nb + min(B0 + 31, g.nb - 1);
+            wait_flag(to.flags, lfirst >> 5, to.epoch);
+            if ((llast >> 5) != (lfirst >> 5)) wait_flag(to.flags, llast >> 5, to.epoch);
+        }
+        __syncthreads();
+    }
     if (INNER && multi && active) {  // KA's record of this chunk
         const float* srcr = crec + (long long)j * RL::REC * NLl + L;
 #pragma unroll
-        for (int f = 0; f < RL::REC; ++f) recs[f * rs + tid] = srcr[(long long)f * NLl];
+        for (int f = 0; f < RL::REC; ++f) recs[f * rs + tid] = __ldcg(srcr + (long long)f * NLl);
     }
-    if (early) pdl_wait();  // separators
+    if (early && !flagged) pdl_wait();  // separators
     pdl_trigger();
 
     float zl[R][C], zr[R][C];
@@ -1085,8 +1133,8 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             for (int q = 0; q < R; ++q)
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    zL[q][c] = has_l ? zsep[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
-                    zR[q][c] = has_r ? zsep[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
+                    zL[q][c] = has_l ? __ldcg(zsep + ((long long)(J - 1) * R * C + q * C + c) * NLl + L) : 0.f;
+                    zR[q][c] = has_r ? __ldcg(zsep + ((long long)J * R * C + q * C + c) * NLl + L) : 0.f;
                 }
             // The boundary values are stored BEFORE the solve: nvcc 12.9 was seen to
             // reuse the register holding `nw` as the back-substitution loop counter
@@ -1137,7 +1185,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         int bmin, bmax;
         covering(g, xa + xl, bmin, bmax);
         // owner CTA = ceil((bmax - 31) / step) (0 if bmax <= 31), tested without a division
-        const int bx = blockIdx.x, q = bmax - 31;
+        const int bx = bxi, q = bmax - 31;
         const bool owned = bx == 0 ? q <= 0 : (q > (bx - 1) * to.step && q <= bx * to.step);
         const float inv = 1.0f / (float)(bmax - bmin + 1);
         inv_col[xl] = owned ? inv : -inv;
@@ -1261,6 +1309,8 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             }
         }
     }
+    // flag mode: this grid completes only after KA has (the next pass's KA waits on it)
+    if (flagged) pdl_wait();
 }
 
 // =========================================================== host helpers
@@ -1291,7 +1341,8 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
     const int PB = (g.P + NW - 1) / NW;
     cudaError_t e;
     if (g.P > 1) {
-        const bool fuse = tile_fuse_k2(PSA) && pl.counters != nullptr;
+        const bool flagged = pl.flags != nullptr && !kc && PSA > 1;
+        const bool fuse = pl.counters != nullptr && (flagged || tile_fuse_k2(PSA));
         {
             ProfScope ps("ka_tile", st);
             const size_t smem_ka = (size_t)RL::REC * (NWA * 32 + 1) * sizeof(float);
@@ -1299,8 +1350,18 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             const size_t smem = smem_ka > smem_k2 ? smem_ka : smem_k2;
             e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, NWA), smem, st, g, pl.src,
-                           pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w);
+            static const int jfast = [] {
+                const char* v = std::getenv("SGWLS_KA_JFAST");  // tuning knob: KA grid order
+                return v ? std::atoi(v) : 0;
+            }();
+            static const int ka_late = [] {
+                const char* v = std::getenv("SGWLS_KA_LATE");  // tuning knob: late dependent-launch trigger
+                return v ? std::atoi(v) : 1;
+            }();
+            const dim3 grid = jfast ? dim3(PSA, (NL + 31) / 32) : dim3((NL + 31) / 32, PSA);
+            e = launch_pdl(ka_tile<R, C, CG>, grid, dim3(32, NWA), smem, st, g, pl.src,
+                           pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w,
+                           flagged ? pl.flags : nullptr, pl.epoch, jfast | ((flagged && ka_late) ? 2 : 0));
             if (e != cudaSuccess) return e;
         }
         if (PSA > 1 && !fuse) {
@@ -1331,21 +1392,28 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         constexpr int RW = rows_per_chunk(R, C);
         const int ncol = 31 * g.tau + 2 * g.r + 1;
         const size_t smem = kb_smem_bytes<R, C>(!kc, NW, NW * RW, ncol);
-        const bool k2_separate = g.P > 1 && PSA > 1 && !(tile_fuse_k2(PSA) && pl.counters != nullptr);
+        const bool flagged = g.P > 1 && pl.flags != nullptr && !kc && PSA > 1;
+        const bool k2_separate = g.P > 1 && PSA > 1 && !flagged && !(tile_fuse_k2(PSA) && pl.counters != nullptr);
+        static const int kb_jfast = [] {
+            const char* v = std::getenv("SGWLS_KB_JFAST");  // tuning knob: KB grid order
+            return v ? std::atoi(v) : 0;
+        }();
         static const int rowmaj_odd = [] {
             const char* v = std::getenv("SGWLS_ROWMAJ_ODD");  // tuning knob
             return v ? std::atoi(v) : 1;
         }();
-        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, k2_separate ? 1 : 0, rowmaj_odd};
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, k2_separate ? 1 : 0, rowmaj_odd,
+                   flagged ? pl.flags : nullptr, pl.epoch, kb_jfast};
+        const dim3 kgrid = kb_jfast ? dim3(PB, pl.ncta, g.batch) : dim3(pl.ncta, PB, g.batch);
         if (kc) {
             e = cudaFuncSetAttribute(kb_tile<R, C, CG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            e = launch_pdl(kb_tile<R, C, CG, false>, dim3(pl.ncta, PB, g.batch), dim3(32, NW), smem, st, g, pl.src,
+            e = launch_pdl(kb_tile<R, C, CG, false>, kgrid, dim3(32, NW), smem, st, g, pl.src,
                            pl.guid, (const float*)pl.sep, (const float*)nullptr, to, pl.err, *pl.w);
         } else {
             e = cudaFuncSetAttribute(kb_tile<R, C, CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
-            e = launch_pdl(kb_tile<R, C, CG, true>, dim3(pl.ncta, PB, g.batch), dim3(32, NW), smem, st, g, pl.src,
+            e = launch_pdl(kb_tile<R, C, CG, true>, kgrid, dim3(32, NW), smem, st, g, pl.src,
                            pl.guid, (const float*)pl.z, (const float*)pl.crec, to, pl.err, *pl.w);
         }
         if (e != cudaSuccess) return e;

@@ -17,6 +17,9 @@ CASES = [  # (h, w, c, r, tau, lam, T)
     (200, 140, 2, 2, 2, 400.0, 3),
     (181, 99, 1, 3, 2, 900.0, 2),
     (140, 77, 1, 4, 5, 100.0, 2),
+    # tall lines: long reduced systems
+    (4100, 40, 2, 1, 2, 400.0, 2),
+    (9000, 36, 1, 1, 1, 900.0, 1),
 ]
 port = CpuOracle("port")
 rng = np.random.default_rng(5)
