@@ -140,6 +140,44 @@ int sgwls_b200_profile_read(char* json, size_t len);
 void sgwls_b200_profile_collect(void);
 
 /* Library version string. */
+
+/* ---- application pipelines (proj/include/sgwls/apps.hpp, proj/src/apps.cpp) ----
+ * The reference's four callers of the filter, with every stage on the device:
+ * one upload, the smooth() / interpolate_sparse() passes and the elementwise
+ * stages (sgwls_apps.cu) on device buffers, one download.  Same parameters,
+ * presets and error texts as the reference; fp32 samples. */
+
+/* ToneMapParams (proj/include/sgwls/apps.hpp:21-30) */
+typedef struct sgwls_b200_tonemap_params {
+    double lambdas[3];           /* {5, 40, 320} */
+    double detail_weights[3];    /* {1, 1, 1} */
+    double target_log_range;     /* 2 */
+    sgwls_b200_config smoothing; /* tonemap_layer_preset(5); lambda set per stage */
+} sgwls_b200_tonemap_params;
+
+/* presets (proj/src/apps.cpp:8-56) */
+void sgwls_b200_enhance_preset(sgwls_b200_config* cfg);
+void sgwls_b200_tonemap_layer_preset(double lambda, sgwls_b200_config* cfg);
+int sgwls_b200_upsample_preset(int factor, sgwls_b200_config* cfg, char* err, size_t errlen);
+void sgwls_b200_colorize_preset(sgwls_b200_config* cfg);
+void sgwls_b200_tonemap_params_default(sgwls_b200_tonemap_params* p);
+
+/* detail_enhance (proj/src/apps.cpp:58-64): clamp(base + boost*(img - base)), base = smooth(img, img) */
+int sgwls_b200_detail_enhance(const float* img, int width, int height, int channels, double boost,
+                              const sgwls_b200_config* cfg, float* out, char* err, size_t errlen);
+/* tone_map (proj/src/apps.cpp:66-109); channels 1 or 3, out like hdr */
+int sgwls_b200_tone_map(const float* hdr, int width, int height, int channels, const sgwls_b200_tonemap_params* p,
+                        float* out, char* err, size_t errlen);
+/* depth_upsample (proj/src/apps.cpp:111-128): lowres low_width x low_height x low_channels (must be 1),
+ * guidance width x height x guidance_channels (1 or 3), out width x height x 1 */
+int sgwls_b200_depth_upsample(const float* lowres, int low_width, int low_height, int low_channels,
+                              const float* guidance, int width, int height, int guidance_channels, int factor,
+                              const sgwls_b200_config* cfg, float* out, char* err, size_t errlen);
+/* colorize (proj/src/apps.cpp:130-155): gray (1 channel), scribbles (3), mask (1), out width x height x 3 */
+int sgwls_b200_colorize(const float* gray, int gray_channels, const float* scribbles, int scribble_channels,
+                        const float* scribble_mask, int width, int height, const sgwls_b200_config* cfg, float* out,
+                        char* err, size_t errlen);
+
 const char* sgwls_b200_version(void);
 
 #ifdef __cplusplus

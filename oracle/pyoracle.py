@@ -171,3 +171,64 @@ def available(kind: str) -> bool:
         return True
     except (FileNotFoundError, OSError, subprocess.CalledProcessError):
         return False
+
+
+class RefApps:
+    """The reference's application pipelines (proj/src/apps.cpp) from
+    oracle/_ref/libsgwls_ref.so: the checker of the device pipelines
+    (paper_1705_01674_b200.apps).  Needs the reference build (this container
+    builds it; the .so travels to the GPU box with the repository)."""
+
+    def __init__(self):
+        self.lib = CpuOracle("reference").lib
+        L = self.lib
+        L.ref_detail_enhance_f32.argtypes = [_P, C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(OracleConfig), _P,
+                                             C.c_char_p, C.c_size_t]
+        L.ref_tone_map_f32.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P, _P, C.c_double, C.POINTER(OracleConfig),
+                                       _P, C.c_char_p, C.c_size_t]
+        L.ref_depth_upsample_f32.argtypes = [_P, C.c_int, C.c_int, C.c_int, _P, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.POINTER(OracleConfig), _P, C.c_char_p, C.c_size_t]
+        L.ref_colorize_f32.argtypes = [_P, _P, _P, C.c_int, C.c_int, C.POINTER(OracleConfig), _P, C.c_char_p,
+                                       C.c_size_t]
+
+    @staticmethod
+    def _call(fn, *args):
+        err = C.create_string_buffer(512)
+        if fn(*args, err, 512):
+            raise OracleError(err.value.decode())
+
+    def detail_enhance(self, img, boost, cfg):
+        a = CpuOracle._hwc(img)
+        h, w, c = a.shape
+        out = np.empty((h, w, c))
+        self._call(self.lib.ref_detail_enhance_f32, a.ctypes.data, w, h, c, float(boost), C.byref(make_config(cfg)),
+                   out.ctypes.data)
+        return out if np.asarray(img).ndim == 3 else out[:, :, 0]
+
+    def tone_map(self, hdr, params):
+        a = CpuOracle._hwc(hdr)
+        h, w, c = a.shape
+        lam = np.asarray(params.lambdas, dtype=np.float64)
+        dw = np.asarray(params.detail_weights, dtype=np.float64)
+        out = np.empty((h, w, c))
+        self._call(self.lib.ref_tone_map_f32, a.ctypes.data, w, h, c, lam.ctypes.data, dw.ctypes.data,
+                   float(params.target_log_range), C.byref(make_config(params.smoothing)), out.ctypes.data)
+        return out if np.asarray(hdr).ndim == 3 else out[:, :, 0]
+
+    def depth_upsample(self, low, guidance, factor, cfg):
+        d = CpuOracle._hwc(low)
+        g = CpuOracle._hwc(guidance)
+        out = np.empty(g.shape[:2])
+        self._call(self.lib.ref_depth_upsample_f32, d.ctypes.data, d.shape[1], d.shape[0], d.shape[2], g.ctypes.data,
+                   g.shape[1], g.shape[0], g.shape[2], int(factor), C.byref(make_config(cfg)), out.ctypes.data)
+        return out
+
+    def colorize(self, gray, scribbles, mask, cfg):
+        g = np.ascontiguousarray(gray, dtype=np.float32)
+        s = np.ascontiguousarray(scribbles, dtype=np.float32)
+        m = np.ascontiguousarray(mask, dtype=np.float32)
+        h, w = g.shape[:2]
+        out = np.empty((h, w, 3))
+        self._call(self.lib.ref_colorize_f32, g.ctypes.data, s.ctypes.data, m.ctypes.data, w, h,
+                   C.byref(make_config(cfg)), out.ctypes.data)
+        return out

@@ -11,6 +11,7 @@
 #include <string>
 #include <vector>
 
+#include "sgwls/apps.hpp"
 #include "sgwls/banded.hpp"
 #include "sgwls/smoother.hpp"
 #include "sgwls/weights.hpp"
@@ -59,6 +60,67 @@ int ref_smooth_f32(const float* target, int width, int height, int channels, con
         const sgwls::Image t = to_img(target, width, height, channels);
         const sgwls::Image g = to_img(guidance, width, height, guidance_channels);
         const sgwls::Image o = sgwls::smooth(t, g, to_cfg(c));
+        std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+// The reference's application pipelines (proj/src/apps.cpp), fp32 inputs
+// promoted to double, double outputs: the parity anchor of the device
+// pipelines (tests/test_apps.py).
+int ref_detail_enhance_f32(const float* img, int width, int height, int channels, double boost,
+                           const oracle_config* c, double* out, char* err, std::size_t errlen) {
+    try {
+        const sgwls::Image o = sgwls::detail_enhance(to_img(img, width, height, channels), boost, to_cfg(c));
+        std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+int ref_tone_map_f32(const float* hdr, int width, int height, int channels, const double* lambdas,
+                     const double* detail_weights, double target_log_range, const oracle_config* smoothing,
+                     double* out, char* err, std::size_t errlen) {
+    try {
+        sgwls::ToneMapParams p;
+        for (int i = 0; i < 3; ++i) {
+            p.lambdas[i] = lambdas[i];
+            p.detail_weights[i] = detail_weights[i];
+        }
+        p.target_log_range = target_log_range;
+        p.smoothing = to_cfg(smoothing);
+        const sgwls::Image o = sgwls::tone_map(to_img(hdr, width, height, channels), p);
+        std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+int ref_depth_upsample_f32(const float* low, int lw, int lh, int lc, const float* guidance, int width, int height,
+                           int gc, int factor, const oracle_config* c, double* out, char* err, std::size_t errlen) {
+    try {
+        const sgwls::Image o = sgwls::depth_upsample(to_img(low, lw, lh, lc), to_img(guidance, width, height, gc),
+                                                     factor, to_cfg(c));
+        std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return 1;
+    }
+}
+
+int ref_colorize_f32(const float* gray, const float* scribbles, const float* mask, int width, int height,
+                     const oracle_config* c, double* out, char* err, std::size_t errlen) {
+    try {
+        const sgwls::Image o = sgwls::colorize(to_img(gray, width, height, 1), to_img(scribbles, width, height, 3),
+                                               to_img(mask, width, height, 1), to_cfg(c));
         std::memcpy(out, o.data.data(), sizeof(double) * o.data.size());
         return 0;
     } catch (const std::exception& e) {

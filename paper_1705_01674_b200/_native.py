@@ -36,6 +36,25 @@ class NativeConfig(C.Structure):
     ]
 
 
+class NativeToneMapParams(C.Structure):
+    """sgwls_b200_tonemap_params (include/sgwls_b200.h), ToneMapParams proj/include/sgwls/apps.hpp:21-30"""
+    _fields_ = [
+        ("lambdas", C.c_double * 3),
+        ("detail_weights", C.c_double * 3),
+        ("target_log_range", C.c_double),
+        ("smoothing", NativeConfig),
+    ]
+
+
+def from_native(n: NativeConfig) -> SmoothConfig:
+    from .config import WeightParams
+    return SmoothConfig(lambda_=n.lambda_, r=n.r, tau=n.tau, iterations=n.iterations,
+                        weight=WeightParams(kind=WeightKind(n.weight_kind), alpha_s=n.alpha_s, alpha_r=n.alpha_r,
+                                            sigma_s=n.sigma_s, sigma_r=n.sigma_r, epsilon=n.epsilon,
+                                            guidance_scale=n.guidance_scale),
+                        first_axis=Axis(n.first_axis), threads=n.threads)
+
+
 def to_native(cfg: SmoothConfig) -> NativeConfig:
     w = cfg.weight
     return NativeConfig(float(cfg.lambda_), int(cfg.r), int(cfg.tau), int(cfg.iterations),
@@ -74,6 +93,20 @@ SIGNATURES = {
     "sgwls_b200_profile_read": (C.c_int, [C.c_char_p, C.c_size_t]),
     "sgwls_b200_profile_collect": (None, []),
     "sgwls_b200_version": (C.c_char_p, []),
+    # application pipelines (proj/src/apps.cpp)
+    "sgwls_b200_enhance_preset": (None, [C.POINTER(NativeConfig)]),
+    "sgwls_b200_tonemap_layer_preset": (None, [C.c_double, C.POINTER(NativeConfig)]),
+    "sgwls_b200_upsample_preset": (C.c_int, [C.c_int, C.POINTER(NativeConfig), C.c_char_p, C.c_size_t]),
+    "sgwls_b200_colorize_preset": (None, [C.POINTER(NativeConfig)]),
+    "sgwls_b200_tonemap_params_default": (None, [C.POINTER(NativeToneMapParams)]),
+    "sgwls_b200_detail_enhance": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_double, C.POINTER(NativeConfig), _P,
+                                            C.c_char_p, C.c_size_t]),
+    "sgwls_b200_tone_map": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.POINTER(NativeToneMapParams), _P,
+                                      C.c_char_p, C.c_size_t]),
+    "sgwls_b200_depth_upsample": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, C.c_int, C.c_int, C.c_int, C.c_int,
+                                            C.POINTER(NativeConfig), _P, C.c_char_p, C.c_size_t]),
+    "sgwls_b200_colorize": (C.c_int, [_P, C.c_int, _P, C.c_int, _P, C.c_int, C.c_int, C.POINTER(NativeConfig), _P,
+                                      C.c_char_p, C.c_size_t]),
 }
 
 

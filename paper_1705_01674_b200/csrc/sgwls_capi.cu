@@ -822,4 +822,218 @@ int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, i
 
 const char* sgwls_b200_version(void) { return "sgwls_b200 0.1.0 (sm_100a)"; }
 
+// ------------------------------------------------ application pipelines
+// proj/src/apps.cpp, every stage on the device (sgwls_apps.cu).
+
+void sgwls_b200_enhance_preset(sgwls_b200_config* c) {  // proj/src/apps.cpp:8-20
+    sgwls_b200_config_default(c);
+    c->lambda = 900.0;
+    c->r = 1;
+    c->tau = 1;
+    c->iterations = 4;
+    c->weight_kind = SGWLS_B200_WEIGHT_FRAC;
+    c->alpha_s = 1.2;
+    c->alpha_r = 1.2;
+    c->guidance_scale = 1.0;
+}
+
+void sgwls_b200_tonemap_layer_preset(double lambda, sgwls_b200_config* c) {  // proj/src/apps.cpp:22-26
+    sgwls_b200_enhance_preset(c);
+    c->lambda = lambda;
+}
+
+int sgwls_b200_upsample_preset(int factor, sgwls_b200_config* c, char* err, size_t errlen) {  // :28-44
+    sgwls_b200_config_default(c);
+    c->r = 4;
+    c->tau = 4;
+    c->iterations = 4;
+    c->weight_kind = SGWLS_B200_WEIGHT_EXP;
+    c->sigma_s = 4.0;
+    c->sigma_r = 3.0;
+    c->guidance_scale = 255.0;
+    switch (factor) {
+        case 2: c->lambda = 100.0; return SGWLS_B200_OK;
+        case 4: c->lambda = 200.0; return SGWLS_B200_OK;
+        case 8: c->lambda = 400.0; return SGWLS_B200_OK;
+        default:
+            put_err(err, errlen, "upsample_preset: published lambdas cover factors 2, 4 and 8");
+            return SGWLS_B200_EINVAL;
+    }
+}
+
+void sgwls_b200_colorize_preset(sgwls_b200_config* c) {  // proj/src/apps.cpp:46-56
+    sgwls_b200_config_default(c);
+    c->lambda = 900.0;
+    c->r = 4;
+    c->tau = 2;
+    c->iterations = 4;
+    c->weight_kind = SGWLS_B200_WEIGHT_EXP;
+    c->sigma_s = 4.0;
+    c->sigma_r = 2.0;
+    c->guidance_scale = 255.0;
+}
+
+void sgwls_b200_tonemap_params_default(sgwls_b200_tonemap_params* p) {  // proj/include/sgwls/apps.hpp:21-30
+    p->lambdas[0] = 5.0;
+    p->lambdas[1] = 40.0;
+    p->lambdas[2] = 320.0;
+    p->detail_weights[0] = p->detail_weights[1] = p->detail_weights[2] = 1.0;
+    p->target_log_range = 2.0;
+    sgwls_b200_tonemap_layer_preset(5.0, &p->smoothing);
+}
+
+int sgwls_b200_detail_enhance(const float* img, int width, int height, int channels, double boost,
+                              const sgwls_b200_config* cfg, float* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        // base = smooth(img, img, cfg): the configuration is validated first
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(1, width, height, channels, channels, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        cudaStream_t st = cudaStreamPerThread;
+        const size_t n = (size_t)width * height * channels;
+        DevBuf dimg, dbase, dout;
+        dimg.alloc(n, st);
+        dbase.alloc(n, st);
+        dout.alloc(n, st);
+        CK(cudaMemcpyAsync(dimg.p, img, n * 4, cudaMemcpyHostToDevice, st));
+        ErrWord ew(st);
+        run_smooth(dimg.p, dimg.p, 1, width, height, channels, channels, cfg, dbase.p, ew.d, st);
+        CK(launch_detail(dimg.p, dbase.p, (float)boost, dout.p, (long long)n, st));
+        CK(cudaMemcpyAsync(out, dout.p, n * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_tone_map(const float* hdr, int width, int height, int channels, const sgwls_b200_tonemap_params* p,
+                        float* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (channels != 1 && channels != 3) throw Fail{SGWLS_B200_EINVAL, "luminance needs 1 or 3 channels"};
+        require_device();
+        cudaStream_t st = cudaStreamPerThread;
+        const long long npx = (long long)(width > 0 ? width : 0) * (height > 0 ? height : 0);
+        const size_t n = (size_t)npx * channels;
+        DevBuf dhdr, dlum, dout, dlev[4];
+        DevBuf flags;  // [bad | min | max | anchor]
+        dhdr.alloc(n, st);
+        dout.alloc(n, st);
+        dlum.alloc(npx, st);
+        for (auto& b : dlev) b.alloc(npx, st);
+        flags.alloc(4, st);
+        unsigned* dflags = reinterpret_cast<unsigned*>(flags.p);
+        const unsigned init[4] = {0u, 0xffffffffu, 0u, 0u};
+        CK(cudaMemcpyAsync(dflags, init, sizeof init, cudaMemcpyHostToDevice, st));
+        if (npx > 0) {
+            CK(cudaMemcpyAsync(dhdr.p, hdr, n * 4, cudaMemcpyHostToDevice, st));
+            CK(launch_luma_log(dhdr.p, channels, dlum.p, dlev[0].p, npx, dflags, st));
+            unsigned bad = 0;
+            CK(cudaMemcpyAsync(&bad, dflags, sizeof bad, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (bad) throw Fail{SGWLS_B200_EINVAL, "tone_map: luminance must be strictly positive"};
+        }
+        // level_{i+1} = smooth(level_i, log_lum, smoothing with lambda_i)   (proj/src/apps.cpp:78-88)
+        ErrWord ew(st);
+        for (int i = 0; i < 3; ++i) {
+            sgwls_b200_config c = p->smoothing;
+            c.lambda = p->lambdas[i];
+            std::string msg;
+            int rc = validate_cfg(&c, msg);
+            if (rc) throw Fail{rc, msg};
+            rc = check_shape(1, width, height, 1, 1, msg);
+            if (rc) throw Fail{rc, msg};
+            run_smooth(dlev[i].p, dlev[0].p, 1, width, height, 1, 1, &c, dlev[i + 1].p, ew.d, st);
+        }
+        const float* lev[4] = {dlev[0].p, dlev[1].p, dlev[2].p, dlev[3].p};
+        const float dw[3] = {(float)p->detail_weights[0], (float)p->detail_weights[1], (float)p->detail_weights[2]};
+        CK(launch_tone_out(dhdr.p, channels, dlum.p, lev, dflags + 1, (float)p->target_log_range, dw, dout.p, npx,
+                           st));
+        CK(cudaMemcpyAsync(out, dout.p, n * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_depth_upsample(const float* lowres, int low_width, int low_height, int low_channels,
+                              const float* guidance, int width, int height, int guidance_channels, int factor,
+                              const sgwls_b200_config* cfg, float* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        // checks in the reference's order (proj/src/apps.cpp:113-116, then luminance(guidance))
+        if (low_channels != 1) throw Fail{SGWLS_B200_EINVAL, "depth_upsample: depth must be single-channel"};
+        if (factor < 1) throw Fail{SGWLS_B200_EINVAL, "depth_upsample: factor must be >= 1"};
+        if (width != low_width * factor || height != low_height * factor)
+            throw Fail{SGWLS_B200_EINVAL, "depth_upsample: guidance must be exactly factor times the depth size"};
+        if (guidance_channels != 1 && guidance_channels != 3)
+            throw Fail{SGWLS_B200_EINVAL, "luminance needs 1 or 3 channels"};
+        // the projected field is 0/1 by construction; an empty one is the reference's error
+        if ((long long)low_width * low_height <= 0) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(1, width, height, 2, 1, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        cudaStream_t st = cudaStreamPerThread;
+        const long long npx = (long long)width * height, nlow = (long long)low_width * low_height;
+        DevBuf dlow, dguid, dlum, dval, dmask, dout;
+        dlow.alloc(nlow, st);
+        dguid.alloc(npx * guidance_channels, st);
+        dval.alloc(npx, st);
+        dmask.alloc(npx, st);
+        dout.alloc(npx, st);
+        CK(cudaMemcpyAsync(dlow.p, lowres, nlow * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dguid.p, guidance, npx * guidance_channels * 4, cudaMemcpyHostToDevice, st));
+        const float* g = dguid.p;
+        if (guidance_channels == 3) {
+            dlum.alloc(npx, st);
+            CK(launch_luma(dguid.p, 3, dlum.p, npx, st));
+            g = dlum.p;
+        }
+        CK(cudaMemsetAsync(dval.p, 0, npx * 4, st));
+        CK(cudaMemsetAsync(dmask.p, 0, npx * 4, st));
+        CK(launch_scatter_depth(dlow.p, low_width, low_height, factor, width, dval.p, dmask.p, st));
+        ErrWord ew(st);
+        run_sparse(dval.p, dmask.p, g, 1, width, height, 1, 1, cfg, dout.p, nullptr, ew.d, st);
+        CK(cudaMemcpyAsync(out, dout.p, npx * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+    });
+}
+
+int sgwls_b200_colorize(const float* gray, int gray_channels, const float* scribbles, int scribble_channels,
+                        const float* scribble_mask, int width, int height, const sgwls_b200_config* cfg, float* out,
+                        char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (gray_channels != 1) throw Fail{SGWLS_B200_EINVAL, "colorize: gray image must be single-channel"};
+        if (scribble_channels != 3) throw Fail{SGWLS_B200_EINVAL, "colorize: scribbles must be 3-channel"};
+        require_device();
+        cudaStream_t st = cudaStreamPerThread;
+        const long long npx = (long long)(width > 0 ? width : 0) * (height > 0 ? height : 0);
+        DevBuf dgray, dscrib, dmask, duv, dres, dout;
+        dgray.alloc(npx, st);
+        dscrib.alloc(npx * 3, st);
+        dmask.alloc(npx, st);
+        duv.alloc(npx * 2, st);
+        dres.alloc(npx * 2, st);
+        dout.alloc(npx * 3, st);
+        CK(cudaMemcpyAsync(dgray.p, gray, npx * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dscrib.p, scribbles, npx * 3 * 4, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dmask.p, scribble_mask, npx * 4, cudaMemcpyHostToDevice, st));
+        // U and V share the mask and the guidance: one 2-channel interpolate_sparse
+        // (the reference's two calls, proj/src/apps.cpp:151-152, factor identically)
+        CK(launch_colorize_pack(dscrib.p, dmask.p, duv.p, npx, st));
+        if (npx <= 0) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
+        validate_sparse(duv.p, dmask.p, 1, npx, 2, st);
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(1, width, height, 3, 1, msg);
+        if (rc) throw Fail{rc, msg};
+        ErrWord ew(st);
+        run_sparse(duv.p, dmask.p, dgray.p, 1, width, height, 2, 1, cfg, dres.p, nullptr, ew.d, st);
+        CK(launch_colorize_out(dgray.p, dres.p, dout.p, npx, st));
+        CK(cudaMemcpyAsync(out, dout.p, npx * 3 * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+    });
+}
+
 }  // extern "C"

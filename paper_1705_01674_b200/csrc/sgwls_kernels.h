@@ -50,4 +50,16 @@ cudaError_t launch_ratio(const float* packed, float* out, float* und, long long 
 cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C,
                                    unsigned long long* status, cudaStream_t st);
 
+// application-pipeline stages (sgwls_apps.cu, proj/src/apps.cpp)
+cudaError_t launch_detail(const float* img, const float* base, float boost, float* out, long long n, cudaStream_t st);
+cudaError_t launch_luma(const float* img, int C, float* lum, long long n, cudaStream_t st);
+cudaError_t launch_luma_log(const float* hdr, int C, float* lum, float* loglum, long long n, unsigned* bad,
+                            cudaStream_t st);
+cudaError_t launch_tone_out(const float* hdr, int C, const float* lum, const float* const lev[4], unsigned* red,
+                            float target_range, const float dw[3], float* out, long long n, cudaStream_t st);
+cudaError_t launch_scatter_depth(const float* low, int lw, int lh, int f, int W, float* values, float* mask,
+                                 cudaStream_t st);
+cudaError_t launch_colorize_pack(const float* scrib, const float* mask, float* uv, long long n, cudaStream_t st);
+cudaError_t launch_colorize_out(const float* gray, const float* uv, float* out, long long n, cudaStream_t st);
+
 }  // namespace sgwls_b200
