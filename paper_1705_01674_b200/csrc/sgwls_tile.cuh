@@ -124,6 +124,50 @@ __device__ __forceinline__ constexpr int offi(int i, int j, int R) { return i * 
 // that are dead for a given unrolled iteration must still be in bounds
 __host__ __device__ constexpr int cl(int x, int n) { return x < 0 ? 0 : (x >= n ? n - 1 : x); }
 
+// Paired FP32 (sm_100 FFMA2 / FMUL2): two independent elements of a register
+// row per instruction, each rounded exactly like fmaf / __fmul_rn (results are
+// bit-identical to the scalar loop); a scalar operand is a native broadcast
+// (R.F32).  FFMA2 has the FFMA pipe throughput but half the issue slots
+// (scripts/micro/ffma2.cu on B200: 36.7 vs 36.2 T FMA/s alone, 27.3 vs 20.6
+// interleaved with IMADs).  Inside one elimination chain, though, the pairs do
+// not survive the window shifts: ptxas adds moves and spills that cancel the
+// saving (measured -1..+1 % on c2-c5), so SGWLS_FFMA2 defaults to 0.
+#ifndef SGWLS_FFMA2
+#define SGWLS_FFMA2 0
+#endif
+// dst[k] = fma(s, src[k], dst[k]), k < N
+template <int N>
+__device__ __forceinline__ void row_fma(float* dst, float s, const float* src) {
+#pragma unroll
+    for (int k = 0; k + 1 < N; k += 2) {
+#if SGWLS_FFMA2
+        const float2 r = __ffma2_rn(make_float2(src[k], src[k + 1]), make_float2(s, s), make_float2(dst[k], dst[k + 1]));
+        dst[k] = r.x;
+        dst[k + 1] = r.y;
+#else
+        dst[k] = fmaf(s, src[k], dst[k]);
+        dst[k + 1] = fmaf(s, src[k + 1], dst[k + 1]);
+#endif
+    }
+    if (N & 1) dst[N - 1] = fmaf(s, src[N - 1], dst[N - 1]);
+}
+// dst[k] = src[k] * s, k < N
+template <int N>
+__device__ __forceinline__ void row_mul(float* dst, const float* src, float s) {
+#pragma unroll
+    for (int k = 0; k + 1 < N; k += 2) {
+#if SGWLS_FFMA2
+        const float2 r = __fmul2_rn(make_float2(src[k], src[k + 1]), make_float2(s, s));
+        dst[k] = r.x;
+        dst[k + 1] = r.y;
+#else
+        dst[k] = src[k] * s;
+        dst[k + 1] = src[k + 1] * s;
+#endif
+    }
+    if (N & 1) dst[N - 1] = src[N - 1] * s;
+}
+
 // squared 2-D distance of the edge (q - t, q), q at in-row index jj (regular band)
 __host__ __device__ constexpr int edge_d2(int jj, int t) {
     return jj >= t ? t * t : 1 + (t - 1 - 2 * jj) * (t - 1 - 2 * jj);
@@ -282,25 +326,28 @@ struct Win {
 #pragma unroll
         for (int i = 1; i <= R; ++i) {
             e[i] = fmaf(cc[i], e[0], e[i]);
-#pragma unroll
-            for (int c = 0; c < C; ++c) g[i][c] = fmaf(cc[i], g[0][c], g[i][c]);
+            row_fma<C>(g[i], cc[i], g[0]);
 #pragma unroll
             for (int k2 = i + 1; k2 <= R; ++k2) A[i][k2] = fmaf(A[0][i], cc[k2], A[i][k2]);
-            if (SPIKE) {
-#pragma unroll
-                for (int mm = 0; mm < R; ++mm) Q[i][mm] = fmaf(cc[i], Q[0][mm], Q[i][mm]);
-            }
+            if (SPIKE) row_fma<R>(Q[i], cc[i], Q[0]);
         }
         if (SPIKE && head) {
+            float d[R];
+            row_mul<R>(d, Q[0], inv);
+            row_fma<R>(he, e[0], d);
 #pragma unroll
-            for (int mm = 0; mm < R; ++mm) {
-                const float d = Q[0][mm] * inv;
-                he[mm] = fmaf(d, e[0], he[mm]);
+            for (int c = 0; c < C; ++c) {
+                float hgc[R];
 #pragma unroll
-                for (int c = 0; c < C; ++c) hg[mm][c] = fmaf(d, g[0][c], hg[mm][c]);
+                for (int mm = 0; mm < R; ++mm) hgc[mm] = hg[mm][c];
+                row_fma<R>(hgc, g[0][c], d);
 #pragma unroll
-                for (int m2 = mm + 1; m2 < R; ++m2) hoff[mm][m2] = fmaf(d, Q[0][m2], hoff[mm][m2]);
+                for (int mm = 0; mm < R; ++mm) hg[mm][c] = hgc[mm];
             }
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm)
+#pragma unroll
+                for (int m2 = mm + 1; m2 < R; ++m2) hoff[mm][m2] = fmaf(d[mm], Q[0][m2], hoff[mm][m2]);
         }
         return inv;
     }
@@ -469,14 +516,10 @@ struct BWin {
 #pragma unroll
         for (int i = mm + 1; i < W2; ++i) {
             e[i] = fmaf(cc[i], e[mm], e[i]);
-#pragma unroll
-            for (int c = 0; c < C; ++c) g[i][c] = fmaf(cc[i], g[mm][c], g[i][c]);
+            row_fma<C>(g[i], cc[i], g[mm]);
 #pragma unroll
             for (int k = i + 1; k < W2; ++k) A[i][k] = fmaf(A[mm][i], cc[k], A[i][k]);
-            if (SPIKE) {
-#pragma unroll
-                for (int q = 0; q < R; ++q) Q[i][q] = fmaf(cc[i], Q[mm][q], Q[i][q]);
-            }
+            if (SPIKE) row_fma<R>(Q[i], cc[i], Q[mm]);
         }
         if (SPIKE && head) {
 #pragma unroll
@@ -912,8 +955,7 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
             const float inv = w.elim(cc, false);
 #pragma unroll
             for (int i = 1; i <= R; ++i) cs[cl(pp, K)][i - 1] = cc[i];
-#pragma unroll
-            for (int c = 0; c < C; ++c) ys[cl(pp, K)][c] = w.g[0][c] * inv;
+            row_mul<C>(ys[cl(pp, K)], w.g[0], inv);
         }
         w.shift();
     }
@@ -923,10 +965,7 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
         if (p < kend) {
 #pragma unroll
             for (int i = 1; i <= R; ++i) {
-                if (p + i < K) {
-#pragma unroll
-                    for (int c = 0; c < C; ++c) ys[p][c] = fmaf(cs[p][i - 1], ys[cl(p + i, K)][c], ys[p][c]);
-                }
+                if (p + i < K) row_fma<C>(ys[p], cs[p][i - 1], ys[cl(p + i, K)]);
             }
         }
     }

@@ -19,6 +19,7 @@
 
 #include "sgwls/smoother.hpp"
 #include "sgwls_b200.h"
+#include "shim_convert.hpp"
 
 namespace sgwls {
 
