@@ -1407,7 +1407,13 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             ProfScope ps("k2_tree", st);
             PassGeom gs = g;
             gs.P = PSA;
-            const int NG = PSA >= 64 ? 16 : 8;
+            static const int ng_env = [] {
+                const char* v = std::getenv("SGWLS_K2_NG");  // tuning knob: warps (groups) of the K2 tree
+                const int n = v ? std::atoi(v) : 0;
+                return n == 4 || n == 8 || n == 16 ? n : 0;
+            }();
+            // measured on B200: 16 warps from 16 super records on (c2 +3 %), 8 below (c1)
+            const int NG = ng_env ? ng_env : (PSA >= 16 ? 16 : 8);
             const size_t sm2 = k2_tree_smem<R, C>(NG);
             e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
             if (e != cudaSuccess) return e;
