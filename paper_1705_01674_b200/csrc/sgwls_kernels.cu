@@ -44,26 +44,29 @@ __global__ void __launch_bounds__(256) k_transpose(const float* __restrict__ in,
     }
 }
 
-// One-channel transpose (the guidance of every row pass): 64x64 tiles, 256
-// threads, 16-byte loads and stores, every load of a thread issued before the
-// shared-memory stores (4 x 16 B in flight per thread); the pitch-65 tile keeps
-// both phases at <= 2-way bank conflicts.  Needs W, H multiples of 4 and
-// 16-byte aligned buffers; edge tiles take the scalar path.
+// One-channel transpose (the guidance of every row pass): TS x TS tiles, 256
+// threads, 16-byte loads and stores, all loads of a thread issued before the
+// shared-memory stores (TS = 64: 4 x 16 B in flight per thread, for large
+// images; TS = 32: one each, 4x the CTAs for small ones).  The pitch-(TS+1)
+// tile keeps both phases at <= 2-way bank conflicts (TS = 32: none).  Needs
+// W, H multiples of 4 and 16-byte aligned buffers; edge tiles go scalar.
+template <int TS>
 __global__ void __launch_bounds__(256) k_transpose1_v4(const float* __restrict__ in, float* __restrict__ out, int H,
                                                        int W, long long stride) {
-    __shared__ float tile[64][65];
-    const int x0 = blockIdx.x * 64, y0 = blockIdx.y * 64, img = blockIdx.z;
+    constexpr int TPR = TS / 4, RPP = 256 / TPR, IT = TS / RPP;  // float4 per row, rows per sweep, sweeps
+    __shared__ float tile[TS][TS + 1];
+    const int x0 = blockIdx.x * TS, y0 = blockIdx.y * TS, img = blockIdx.z;
     const float* ii = in + img * stride;
     float* oo = out + img * stride;
-    const int t = threadIdx.x, r16 = t >> 4, c16 = t & 15;
-    if (x0 + 64 <= W && y0 + 64 <= H) {
-        float4 v[4];
+    const int t = threadIdx.x, rr = t / TPR, cc = t % TPR;
+    if (x0 + TS <= W && y0 + TS <= H) {
+        float4 v[IT];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-            v[i] = __ldg(reinterpret_cast<const float4*>(ii + (long long)(y0 + r16 + 16 * i) * W + x0) + c16);
+        for (int i = 0; i < IT; ++i)
+            v[i] = __ldg(reinterpret_cast<const float4*>(ii + (long long)(y0 + rr + RPP * i) * W + x0) + cc);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            float* d = &tile[r16 + 16 * i][4 * c16];
+        for (int i = 0; i < IT; ++i) {
+            float* d = &tile[rr + RPP * i][4 * cc];
             d[0] = v[i].x;
             d[1] = v[i].y;
             d[2] = v[i].z;
@@ -71,20 +74,20 @@ __global__ void __launch_bounds__(256) k_transpose1_v4(const float* __restrict__
         }
         __syncthreads();
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int x = r16 + 16 * i;
-            const float4 o = make_float4(tile[4 * c16][x], tile[4 * c16 + 1][x], tile[4 * c16 + 2][x], tile[4 * c16 + 3][x]);
-            reinterpret_cast<float4*>(oo + (long long)(x0 + x) * H + y0)[c16] = o;
+        for (int i = 0; i < IT; ++i) {
+            const int x = rr + RPP * i;
+            const float4 o = make_float4(tile[4 * cc][x], tile[4 * cc + 1][x], tile[4 * cc + 2][x], tile[4 * cc + 3][x]);
+            reinterpret_cast<float4*>(oo + (long long)(x0 + x) * H + y0)[cc] = o;
         }
     } else {
-        const int nx = min(64, W - x0), ny = min(64, H - y0);
-        for (int i = t; i < 64 * 64; i += 256) {
-            const int yy = i >> 6, xx = i & 63;
+        const int nx = min(TS, W - x0), ny = min(TS, H - y0);
+        for (int i = t; i < TS * TS; i += 256) {
+            const int yy = i / TS, xx = i % TS;
             if (yy < ny && xx < nx) tile[yy][xx] = __ldg(ii + (long long)(y0 + yy) * W + x0 + xx);
         }
         __syncthreads();
-        for (int i = t; i < 64 * 64; i += 256) {
-            const int xx = i >> 6, yy = i & 63;
+        for (int i = t; i < TS * TS; i += 256) {
+            const int xx = i / TS, yy = i % TS;
             if (yy < ny && xx < nx) oo[(long long)(x0 + xx) * H + y0 + yy] = tile[yy][xx];
         }
     }
@@ -163,13 +166,15 @@ cudaError_t launch_transpose(const float* in, float* out, int H, int W, int C, i
     dim3 grid((W + 31) / 32, (H + 31) / 32, batch);
     ProfScope ps("transpose", st);
     const long long stride = (long long)H * W * C;
-    // 64x64 tiles only when they fill the GPU (>= 8 per SM): c5 guidance 165 -> 89 us;
-    // a 1920x1080 guidance (510 tiles) is faster with the 32x32 kernel's 2040 CTAs
-    const long long tiles64 = (long long)((W + 63) / 64) * ((H + 63) / 64) * batch;
-    const bool v4 = C == 1 && W % 4 == 0 && H % 4 == 0 && tiles64 >= 148 * 8 &&
+    const bool v4 = C == 1 && W % 4 == 0 && H % 4 == 0 &&
                     ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
     if (v4) {
-        k_transpose1_v4<<<dim3((W + 63) / 64, (H + 63) / 64, batch), 256, 0, st>>>(in, out, H, W, stride);
+        // 64x64 tiles when they fill the GPU (>= 8 per SM; c5 guidance 165 -> 89 us), else 32x32
+        const long long tiles64 = (long long)((W + 63) / 64) * ((H + 63) / 64) * batch;
+        if (tiles64 >= 148 * 8)
+            k_transpose1_v4<64><<<dim3((W + 63) / 64, (H + 63) / 64, batch), 256, 0, st>>>(in, out, H, W, stride);
+        else
+            k_transpose1_v4<32><<<dim3((W + 31) / 32, (H + 31) / 32, batch), 256, 0, st>>>(in, out, H, W, stride);
         return cudaGetLastError();
     }
     switch (C) {

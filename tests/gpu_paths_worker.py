@@ -17,6 +17,7 @@ CASES = [  # (h, w, c, r, tau, lam, T)
     (200, 140, 2, 2, 2, 400.0, 3),
     (181, 99, 1, 3, 2, 900.0, 2),
     (140, 77, 1, 4, 5, 100.0, 2),
+    (100, 68, 1, 1, 2, 400.0, 2),  # W, H multiples of 4, not of 32: vectorised transpose with edge tiles
     # tall lines: long reduced systems
     (4100, 40, 2, 1, 2, 400.0, 2),
     (9000, 36, 1, 1, 1, 900.0, 1),
