@@ -141,6 +141,32 @@ void sgwls_b200_profile_collect(void);
 
 /* Library version string. */
 
+/* ---- row-slab mode: one Column pass of an image split into row slabs ----
+ * (one slab per GPU; paper_1705_01674_b200/sharded.py).  The
+ * band solves are partitioned exactly across slabs: phase A computes each
+ * slab's chunk records and ONE slab record per band (record_floats floats,
+ * layout [field][band]); the caller all-gathers the records of the nslabs
+ * slabs back to back ([slab][field][band]); phase B solves the slab separators
+ * and finishes the pass.  Only the slab records cross GPUs, never image data.
+ * d_src: the slab's rows x width x channels; d_guid: the slab's guidance rows,
+ * with row -1 (the previous slab's last row) readable when islab > 0; d_work:
+ * work_floats floats kept between the phases; d_out: rows x width x channels
+ * (caller layout, not transposed).  row0 (global row of the slab's first row)
+ * must be even.  NaN guidance is not reported in this mode. */
+/* out[b][x][y][c] = in[b][y][x][c] on device buffers (width x height -> height x width), stream-ordered */
+int sgwls_b200_transpose_device(const float* d_in, float* d_out, int batch, int width, int height, int channels,
+                                void* stream, char* err, size_t errlen);
+int sgwls_b200_slab_sizes(int width, int rows, int channels, int guidance_channels, int nslabs,
+                          const sgwls_b200_config* cfg, size_t* work_floats, size_t* record_floats, char* err,
+                          size_t errlen);
+int sgwls_b200_slab_pass_a(const float* d_src, const float* d_guidance, int width, int rows, int channels,
+                           int guidance_channels, int row0, int nslabs, int islab, const sgwls_b200_config* cfg,
+                           float* d_work, float* d_record, void* stream, char* err, size_t errlen);
+int sgwls_b200_slab_pass_b(const float* d_src, const float* d_guidance, int width, int rows, int channels,
+                           int guidance_channels, int row0, int nslabs, int islab, const sgwls_b200_config* cfg,
+                           float* d_work, const float* d_records, float* d_out, void* stream, char* err,
+                           size_t errlen);
+
 /* ---- application pipelines (proj/include/sgwls/apps.hpp, proj/src/apps.cpp) ----
  * The reference's four callers of the filter, with every stage on the device:
  * one upload, the smooth() / interpolate_sparse() passes and the elementwise

@@ -609,6 +609,90 @@ int guarded(char* err, size_t errlen, F&& f) {
     }
 }
 
+// ---------------------------------------------------------- row-slab mode
+// One Column pass of an image split into row slabs (one per GPU): layout of
+// the caller-provided workspace and the launch description of both phases
+// (sgwls_tile.cuh "row-slab mode", sharded.py).
+struct SlabLayout {
+    AxisPlan ap;
+    size_t crec = 0, srec = 0, rsc = 0, zext = 0, sepext = 0, zg = 0, bsg = 0, total = 0, record = 0;
+};
+
+SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_config* cfg, int nslabs) {
+    SlabLayout L;
+    L.ap = plan_axis(rows, width, C, Cg, cfg->r, cfg->tau, 1);
+    if (!L.ap.fast)
+        throw Fail{SGWLS_B200_EUNSUPPORTED, "sgwls_b200: row-slab mode needs the tiled path (r <= 4, 1 or 3 guidance "
+                                            "channels, width >= 2r+1)"};
+    const size_t NL = L.ap.g.nb, r = cfg->r, REC = rec_floats(cfg->r, C), RS = rs_floats(cfg->r, C);
+    const size_t P = L.ap.g.P, NWA = L.ap.kc ? L.ap.nwa : L.ap.nw, PS = (P + NWA - 1) / NWA;
+    const size_t G = nslabs > 1 ? nslabs - 1 : 1;
+    size_t off = 0;
+    auto take = [&](size_t n) {
+        const size_t o = off;
+        off += (n + 31) & ~(size_t)31;
+        return o;
+    };
+    L.crec = take(P * REC * NL);
+    L.srec = take(PS * REC * NL);
+    L.rsc = take((PS > 1 ? PS - 1 : 1) * r * RS * NL);
+    L.zext = take((PS + 1) * r * C * NL);
+    L.sepext = take((P + 1) * r * C * NL);
+    L.zg = take(G * r * C * NL);
+    L.bsg = take(G * r * RS * NL);
+    L.total = off;
+    L.record = REC * NL;
+    return L;
+}
+
+void slab_check(int width, int rows, int C, int Cg, int row0, int nslabs, int islab, const sgwls_b200_config* cfg) {
+    std::string msg;
+    int rc = validate_cfg(cfg, msg);
+    if (rc) throw Fail{rc, msg};
+    rc = check_shape(1, width, rows, C, Cg, msg);
+    if (rc) throw Fail{rc, msg};
+    if (nslabs < 1 || islab < 0 || islab >= nslabs)
+        throw Fail{SGWLS_B200_EINVAL, "sgwls_b200: slab index out of range"};
+    if (row0 & 1) throw Fail{SGWLS_B200_EINVAL, "sgwls_b200: slab row offset must be even (serpentine parity)"};
+}
+
+PassLaunch slab_launch(const SlabLayout& L, const float* src, const float* guid, int row0, int nslabs, int islab,
+                       float* work, const WeightDev* wd, int C) {
+    const AxisPlan& ap = L.ap;
+    PassLaunch pl;
+    pl.geom = ap.g;
+    pl.geom.has_prev = islab > 0;
+    pl.geom.has_next = islab < nslabs - 1;
+    pl.geom.row0 = row0;
+    pl.bx = ap.bx;
+    pl.fast = 1;
+    pl.step = ap.step;
+    pl.ncta = ap.ncta;
+    pl.nw = ap.nw;
+    pl.nwa = ap.nwa;
+    pl.kc = ap.kc;
+    pl.nph = ap.nph;
+    pl.kmax = ap.kmax;
+    pl.src = src;
+    pl.guid = guid;
+    pl.w = wd;
+    pl.err = nullptr;
+    pl.U = nullptr;
+    const size_t NL = ap.g.nb, rC = (size_t)ap.g.r * C;
+    pl.crec = work + L.crec;
+    pl.rec = work + L.srec;
+    pl.rs = work + L.rsc;
+    pl.z = work + L.zext + rC * NL;      // one slot in front: z[-1]
+    pl.sep = work + L.sepext + rC * NL;  // one slot in front: sep[-1]
+    pl.zg = work + L.zg;
+    pl.bsg = work + L.bsg;
+    pl.nslab = nslabs;
+    pl.islab = islab;
+    pl.transpose_out = 0;
+    pl.out = nullptr;
+    return pl;
+}
+
 }  // namespace
 
 extern "C" {
@@ -821,6 +905,61 @@ int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, i
 }
 
 const char* sgwls_b200_version(void) { return "sgwls_b200 0.1.0 (sm_100a)"; }
+
+// ------------------------------------------------------------ row-slab mode
+
+int sgwls_b200_transpose_device(const float* d_in, float* d_out, int batch, int width, int height, int channels,
+                                void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (batch < 1 || width < 1 || height < 1 || channels < 1 || channels > 4)
+            throw Fail{SGWLS_B200_EINVAL, "sgwls_b200: transpose needs a non-empty image of 1-4 channels"};
+        require_device();
+        CK(launch_transpose(d_in, d_out, height, width, channels, batch, (cudaStream_t)stream));
+    });
+}
+
+int sgwls_b200_slab_sizes(int width, int rows, int channels, int gch, int nslabs, const sgwls_b200_config* cfg,
+                          size_t* work_floats, size_t* record_floats, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        slab_check(width, rows, channels, gch, 0, nslabs, 0, cfg);
+        const SlabLayout L = slab_layout(width, rows, channels, gch, cfg, nslabs);
+        if (work_floats) *work_floats = L.total;
+        if (record_floats) *record_floats = L.record;
+    });
+}
+
+int sgwls_b200_slab_pass_a(const float* d_src, const float* d_guid, int width, int rows, int channels, int gch,
+                           int row0, int nslabs, int islab, const sgwls_b200_config* cfg, float* d_work,
+                           float* d_record, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        slab_check(width, rows, channels, gch, row0, nslabs, islab, cfg);
+        require_device();
+        const SlabLayout L = slab_layout(width, rows, channels, gch, cfg, nslabs);
+        WeightDev wd;
+        build_weights(cfg, wd);
+        PassLaunch pl = slab_launch(L, d_src, d_guid, row0, nslabs, islab, d_work, &wd, channels);
+        pl.slab_phase = 1;
+        pl.slabrec = d_record;
+        CK(launch_pass(pl, (cudaStream_t)stream));
+    });
+}
+
+int sgwls_b200_slab_pass_b(const float* d_src, const float* d_guid, int width, int rows, int channels, int gch,
+                           int row0, int nslabs, int islab, const sgwls_b200_config* cfg, float* d_work,
+                           const float* d_records, float* d_out, void* stream, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        slab_check(width, rows, channels, gch, row0, nslabs, islab, cfg);
+        require_device();
+        const SlabLayout L = slab_layout(width, rows, channels, gch, cfg, nslabs);
+        WeightDev wd;
+        build_weights(cfg, wd);
+        PassLaunch pl = slab_launch(L, d_src, d_guid, row0, nslabs, islab, d_work, &wd, channels);
+        pl.slab_phase = 2;
+        pl.slabrec = const_cast<float*>(d_records);
+        pl.out = d_out;
+        CK(launch_pass(pl, (cudaStream_t)stream));
+    });
+}
 
 // ------------------------------------------------ application pipelines
 // proj/src/apps.cpp, every stage on the device (sgwls_apps.cu).

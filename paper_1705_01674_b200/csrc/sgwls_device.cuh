@@ -55,6 +55,13 @@ struct PassGeom {
     long long img_stride;   // floats per image of the target layout (Hl*Wl*C)
     long long gimg_stride;  // floats per image of the guidance layout
     unsigned tau_mul;       // ceil(2^32 / tau) (tau > 1): exact x / tau for 0 <= x < 2^28
+    // Row-slab mode (tiled path, a Column pass over rows [row0, row0 + Hl) of a
+    // taller image, sharded.py): the bands continue above (has_prev: the local
+    // chunk 0 couples to the previous slab's last separator, whose guidance row
+    // is readable at row -1) and/or below (has_next: the local last chunk ends
+    // in a separator shared with the next slab).  0/0 for an ordinary pass.
+    int has_prev, has_next;
+    int row0;               // global row of local row 0 (error positions)
 };
 
 __host__ __device__ __forceinline__ unsigned tau_multiplier(int tau) {

@@ -37,6 +37,15 @@ struct PassLaunch {
     // The flags are zeroed once per call; pass p uses epoch p + 1.
     int* flags = nullptr;
     int epoch = 0;
+    // tiled path, row-slab mode (geom.has_prev / has_next, sgwls_tile.cuh):
+    // 1 = phase A (KA, then this slab's record -> slabrec), 2 = phase B (slabrec
+    // = all nslab records; separators, KC, KB); z and sep then carry one slot in
+    // front (the previous slab's separator)
+    int slab_phase = 0;
+    float* slabrec = nullptr;
+    int nslab = 1, islab = 0;
+    float* zg = nullptr;   // nslab-1 slab separators
+    float* bsg = nullptr;  // their back-substitution rows
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);

@@ -194,7 +194,7 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
     for (int i = 0; i < R; ++i) {
         const int jj = M - R + i;
         const int y = y0 - 1;
-        if (y >= 0) {
+        if (y >= 0 || g.has_prev) {
             const int co = (y & 1) ? (M - 1 - jj) : jj;
             const float* p = G + ((long long)y * g.Wl + lo + co) * CG;
 #pragma unroll
@@ -265,8 +265,8 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
         for (int k = 0; k < K; ++k)
 #pragma unroll
             for (int t = 1; t <= R; ++t) {
-                const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
-                bad = (!(in.w[k][t - 1] >= 0.f) && exists) ? min(bad, y0 * M + k - t) : bad;
+                const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0 || g.has_prev);
+                bad = (!(in.w[k][t - 1] >= 0.f) && exists) ? min(bad, (g.row0 + y0) * M + k - t) : bad;
             }
         if (bad != 0x7fffffff) atomicMin(err, ((unsigned long long)(unsigned)line << 32) | (unsigned)bad);
     }
@@ -857,7 +857,7 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows,
                                  nullptr, L);
         // every chunk record also goes to HBM for KC / KB (nothing downstream redoes the spike-forward)
-        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0, j == g.P - 1, nrows * M, rec, rs,
+        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0 || g.has_prev, j == g.P - 1 && !g.has_next, nrows * M, rec, rs,
                                           crec + (long long)j * RL::REC * NL + L, (long long)NL);
     }
     __syncthreads();
@@ -865,7 +865,8 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     const int PS = (g.P + NW - 1) / NW;
     if (wid == 0 && L < NL) {
         const long long NLl = NL;
-        reduce_super<R, C>(sm + lane, rs, 32, nw, J == 0, J == PS - 1, srec + (long long)J * RL::REC * NLl + L, NLl);
+        reduce_super<R, C>(sm + lane, rs, 32, nw, J == 0 && !g.has_prev, J == PS - 1 && !g.has_next,
+                           srec + (long long)J * RL::REC * NLl + L, NLl);
     }
     if (counters == nullptr) return;
     // ---- the last tile of this band group to finish solves the group's
@@ -900,7 +901,7 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
 // FULL_INNER: full chunk that is not the band's last (kv = K, kend = K - R at
 // compile time); otherwise the general predicated form.
 template <int R, int C, int CG, int RW, bool FULL_INNER>
-__device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>& in, float lam, int j, bool lastc,
+__device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left, bool lastc,
                                                      int kv, int kend, const float (&zl)[R][C],
                                                      const float (&zr)[R][C], float (&cs)[RW * (2 * R + 1)][R],
                                                      float (&ys)[RW * (2 * R + 1)][C]) {
@@ -910,6 +911,9 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
         kend = K - R;
         lastc = false;
     }
+    // the chunk's separator (known, zr) is its last R valid positions; a short
+    // chunk that is not the band's last occurs in row-slab mode
+    const int ks = kv - R;
     Win<R, C, false> w;
     w.clear();
     // positions k >= kv (short last chunk) enter as empty rows; the R extra
@@ -917,21 +921,21 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
 #pragma unroll
     for (int k = 0; k < K + R; ++k) {
         if (k < K && k < kv) {
-            const bool kq = !lastc && (k >= K - R);  // known separator position (full chunk)
+            const bool kq = !lastc && (k >= ks);  // known separator position
             if (!kq) {
                 w.e[R] = 1.f;
 #pragma unroll
                 for (int c = 0; c < C; ++c) w.g[R][c] = in.f[cl(k, K)][c];
             } else {
 #pragma unroll
-                for (int c = 0; c < C; ++c) ys[cl(k, K)][c] = zr[cl(k - (K - R), R)][c];
+                for (int c = 0; c < C; ++c) ys[cl(k, K)][c] = zr[cl(k - ks, R)][c];
             }
 #pragma unroll
             for (int t = 1; t <= R; ++t) {
-                const bool pe = (k - t >= 0) || (j > 0);
+                const bool pe = (k - t >= 0) || has_left;
                 if (!pe) continue;
                 const bool pleft = (k - t < 0);
-                const bool pright = kq && (k - t >= K - R);
+                const bool pright = kq && (k - t >= ks);
                 if (pright) continue;
                 const float lw = in.w[cl(k, K)][t - 1];
                 if (!kq && !pleft) {
@@ -945,7 +949,7 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
                     w.e[R - t] += lw;
 #pragma unroll
                     for (int c = 0; c < C; ++c)
-                        w.g[R - t][c] = fmaf(lw, zr[cl(k - (K - R), R)][c], w.g[R - t][c]);
+                        w.g[R - t][c] = fmaf(lw, zr[cl(k - ks, R)][c], w.g[R - t][c]);
                 }
             }
         }
@@ -1025,7 +1029,7 @@ __global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g,
     pdl_trigger();
     if (L >= NL || J >= PSA) return;
     const int nw = min(NWA, g.P - J * NWA);
-    const bool has_l = J > 0, has_r = J < PSA - 1;
+    const bool has_l = J > 0 || g.has_prev, has_r = J < PSA - 1 || g.has_next;
     float zL[R][C], zR[R][C];
 #pragma unroll
     for (int q = 0; q < R; ++q)
@@ -1035,6 +1039,12 @@ __global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g,
             zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
         }
     float* out = sep + (long long)J * NWA * R * C * NLl + L;
+    if (J == 0 && g.has_prev) {  // slab mode: the previous slab's separator, for the first chunk's KB
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) out[((long long)(-R + q) * C + c) * NLl] = zL[q][c];
+    }
     if (has_r) {  // the tile's last separator is the super-separator (stored before the solve, see KB note)
 #pragma unroll
         for (int q = 0; q < R; ++q)
@@ -1049,6 +1059,71 @@ template <int R, int C>
 __host__ inline size_t kc_smem(int NWA, int nty) {
     using RL = Rec<R, C>;
     return (size_t)(NWA > 1 ? NWA - 1 : 1) * R * RL::RS * 32 * nty * sizeof(float);
+}
+
+// ============================================================ row-slab mode
+//
+// A Column pass over a band split into row slabs, one per GPU (sharded.py,
+// SURVEY.md 8(f)-1): the exact partitioned solve one level up.  Phase A per
+// slab: KA as usual (chunk records, super-records), then k2_slab_reduce folds
+// the slab's super-records into ONE slab record per band (the in-tile
+// reduction of reduce_super applied to the whole slab: the Schur block of the
+// slab's last separator, its coupling to the previous slab's, and the update
+// of the latter).  The slab records of all G slabs are all-gathered (G records
+// per band, ~100 B each), and phase B per slab runs k2_slab_solve: the global
+// block-tridiagonal system over the G-1 slab separators (redundantly on every
+// slab, G is tiny), then the slab's own super-separators with its two slab
+// separators as boundary values; then KC / KB as usual.  Only slab records
+// cross GPUs -- never image data.
+template <int R, int C>
+__global__ void __launch_bounds__(128) k2_slab_reduce(const PassGeom g, int PS, const float* __restrict__ srec,
+                                                      float* __restrict__ slabrec) {
+    using RL = Rec<R, C>;
+    const int NL = g.nb * g.batch;
+    const long long NLl = NL;
+    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();  // KA's super-records
+    pdl_trigger();
+    if (L >= NL) return;
+    reduce_super<R, C>(srec + L, NLl, (long long)RL::REC * NLl, PS, !g.has_prev, !g.has_next, slabrec + L, NLl);
+}
+
+// allrec: the G slab records [slab][field][line]; z: this slab's super-separator
+// array with one slot in front (z[-1] = the previous slab's separator, z[PS-1]
+// = this slab's last separator); zg / bsg: global separators / back-substitution
+// scratch; rsc: local back-substitution scratch.
+template <int R, int C>
+__global__ void __launch_bounds__(128) k2_slab_solve(const PassGeom g, int PS, int G, int gi,
+                                                     const float* __restrict__ allrec, const float* __restrict__ srec,
+                                                     float* __restrict__ zg, float* __restrict__ bsg,
+                                                     float* __restrict__ rsc, float* __restrict__ z) {
+    using RL = Rec<R, C>;
+    const int NL = g.nb * g.batch;
+    const long long NLl = NL;
+    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    pdl_wait();
+    pdl_trigger();
+    if (L >= NL) return;
+    float z0[R][C], zL[R][C], zR[R][C];
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) z0[q][c] = 0.f;
+    // the G-1 slab separators (every slab solves the same tiny system)
+    if (G > 1)
+        solve_inner<R, C>(allrec + L, NLl, (long long)RL::REC * NLl, G, false, z0, false, z0, zg + L, NLl, bsg + L,
+                          NLl);
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            zL[q][c] = g.has_prev ? zg[((long long)((gi - 1) * R + q) * C + c) * NLl + L] : 0.f;
+            zR[q][c] = g.has_next ? zg[((long long)(gi * R + q) * C + c) * NLl + L] : 0.f;
+            if (g.has_prev) z[((long long)(-R + q) * C + c) * NLl + L] = zL[q][c];
+            if (g.has_next) z[((long long)((PS - 1) * R + q) * C + c) * NLl + L] = zR[q][c];
+        }
+    solve_inner<R, C>(srec + L, NLl, (long long)RL::REC * NLl, PS, g.has_prev, zL, g.has_next, zR, z + L, NLl,
+                      rsc + L, NLl);
 }
 
 // ===================================================================== KB
@@ -1124,7 +1199,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     // KA's records may be read before the wait only when the predecessor is a
     // K2/KC launch (those trigger after waiting for KA); after a fused or
     // absent K2 the predecessor is KA itself.
-    const bool multi = g.P > 1;
+    const bool multi = g.P > 1 || g.has_prev || g.has_next;  // separators exist
     // ready-flag mode: KA runs the reduced solve per band group and raises a
     // flag; this tile waits for the (at most two) groups its bands belong to.
     // Records and separators are then read through L2 (ld.cg: written by a
@@ -1159,14 +1234,15 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             zl[q][c] = 0.f;
             zr[q][c] = 0.f;
         }
-    const bool lastc = (j == g.P - 1);
+    const bool lastc = (j == g.P - 1) && !g.has_next;
+    const bool has_left = j > 0 || g.has_prev;
     if constexpr (INNER) {
         const int PS = (g.P + NW - 1) / NW;
         __syncthreads();
         // ---- 2. lane-per-band solve of the tile's inner separators with the
         //         two known super-separators as boundary values
         if (wid == 0 && b < g.nb && multi) {
-            const bool has_l = J > 0, has_r = J < PS - 1;
+            const bool has_l = J > 0 || g.has_prev, has_r = J < PS - 1 || g.has_next;
             float zL[R][C], zR[R][C];
 #pragma unroll
             for (int q = 0; q < R; ++q)
@@ -1197,7 +1273,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             for (int q = 0; q < R; ++q)
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    if (j > 0)
+                    if (has_left)
                         zl[q][c] = (wid == 0) ? bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane]
                                               : zint[(((wid - 1) * R + q) * C + c) * 32 + lane];
                     if (!lastc) zr[q][c] = zint[((wid * R + q) * C + c) * 32 + lane];
@@ -1210,7 +1286,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             for (int q = 0; q < R; ++q)
 #pragma unroll
                 for (int c = 0; c < C; ++c) {
-                    if (j > 0) zl[q][c] = zsep[((long long)(j - 1) * R * C + q * C + c) * NLl + L];
+                    if (has_left) zl[q][c] = zsep[((long long)(j - 1) * R * C + q * C + c) * NLl + L];
                     if (!lastc) zr[q][c] = zsep[((long long)j * R * C + q * C + c) * NLl + L];
                 }
         }
@@ -1247,9 +1323,9 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     }
     if (active) {
         if (!lastc && kv == K)
-            chunk_interior_solve<R, C, CG, RW, true>(in, lam, j, lastc, kv, kend, zl, zr, cs, ys);
+            chunk_interior_solve<R, C, CG, RW, true>(in, lam, has_left, lastc, kv, kend, zl, zr, cs, ys);
         else
-            chunk_interior_solve<R, C, CG, RW, false>(in, lam, j, lastc, kv, kend, zl, zr, cs, ys);
+            chunk_interior_solve<R, C, CG, RW, false>(in, lam, has_left, lastc, kv, kend, zl, zr, cs, ys);
     }
     __syncthreads();
     // ---- 4. averaging into the shared output tile, fixed phase order
@@ -1379,7 +1455,30 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
     const int PSA = (g.P + NWA - 1) / NWA;
     const int PB = (g.P + NW - 1) / NW;
     cudaError_t e;
-    if (g.P > 1) {
+    const bool slab = pl.slab_phase != 0;
+    if (pl.slab_phase == 1) {  // row-slab phase A: KA + slab record
+        {
+            ProfScope ps("ka_tile", st);
+            const size_t smem = (size_t)RL::REC * (NWA * 32 + 1) * sizeof(float);
+            e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+            e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, NWA), smem, st, g, pl.src, pl.guid,
+                           pl.rec, pl.rs, pl.z, (int*)nullptr, pl.crec, *pl.w, (int*)nullptr, 0, 0);
+            if (e != cudaSuccess) return e;
+        }
+        ProfScope ps("k2_slab_reduce", st);
+        e = launch_pdl(k2_slab_reduce<R, C>, dim3((NL + 127) / 128), dim3(128), 0, st, g, PSA, (const float*)pl.rec,
+                       pl.slabrec);
+        if (e != cudaSuccess) return e;
+        return cudaGetLastError();
+    }
+    if (pl.slab_phase == 2) {  // row-slab phase B: separators, then KC / KB below
+        ProfScope ps("k2_slab_solve", st);
+        e = launch_pdl(k2_slab_solve<R, C>, dim3((NL + 127) / 128), dim3(128), 0, st, g, PSA, pl.nslab, pl.islab,
+                       (const float*)pl.slabrec, (const float*)pl.rec, pl.zg, pl.bsg, pl.rs, pl.z);
+        if (e != cudaSuccess) return e;
+    }
+    if (g.P > 1 && !slab) {
         const bool flagged = pl.flags != nullptr && !kc && PSA > 1;
         const bool fuse = pl.counters != nullptr && (flagged || tile_fuse_k2(PSA));
         {
@@ -1421,7 +1520,9 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
                            pl.z);
             if (e != cudaSuccess) return e;
         }
-        if (kc) {
+    }
+    if (kc && (g.P > 1 || slab)) {
+        {
             ProfScope ps("kc_inner", st);
             const int nty = 4;
             const size_t smc = kc_smem<R, C>(NWA, nty);
@@ -1438,7 +1539,8 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         const int ncol = 31 * g.tau + 2 * g.r + 1;
         const size_t smem = kb_smem_bytes<R, C>(!kc, NW, NW * RW, ncol);
         const bool flagged = g.P > 1 && pl.flags != nullptr && !kc && PSA > 1;
-        const bool k2_separate = g.P > 1 && PSA > 1 && !flagged && !(tile_fuse_k2(PSA) && pl.counters != nullptr);
+        const bool k2_separate =
+            slab || (g.P > 1 && PSA > 1 && !flagged && !(tile_fuse_k2(PSA) && pl.counters != nullptr));
         static const int kb_jfast = [] {
             const char* v = std::getenv("SGWLS_KB_JFAST");  // tuning knob: KB grid order
             return v ? std::atoi(v) : 0;
