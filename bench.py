@@ -58,6 +58,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--sharded", action="store_true",
                    help="line-slab shard ONE image over the ranks (default for c5 at N>1)")
+    p.add_argument("--shard-mode", default="slabs", choices=["slabs", "transpose"],
+                   help="slabs: row slabs, band solves partitioned across GPUs (slab records + halo rows "
+                        "exchanged); transpose: column windows with an NCCL all-to-all transpose between passes")
     p.add_argument("--local-shards", type=int, default=1,
                    help="with --sharded at N=1: run this many shards in one process (validation)")
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU-baseline sample budget")
@@ -74,7 +77,8 @@ def peaks():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def config_block(wl: WL.Workload, n: int, batch_per_rank: int, sharded: bool = False, shards: int = 1) -> dict:
+def config_block(wl: WL.Workload, n: int, batch_per_rank: int, sharded: bool = False, shards: int = 1,
+                 shard_mode: str = "slabs") -> dict:
     c = wl.cfg
     return {
         "workload": f"{wl.name}: {wl.width}x{wl.height}x{wl.channels}"
@@ -87,7 +91,9 @@ def config_block(wl: WL.Workload, n: int, batch_per_rank: int, sharded: bool = F
         "guidance": "luminance" if wl.name == "c2" else ("per-pair voronoi" if wl.sparse else "input"),
         "l2": "flushed between timed steps (256 MiB memset)",
         "launch": "CUDA graph replay per filter (captured once, SGWLS_B200_GRAPH)",
-        "parallelism": (f"line-slab shards x{shards} (NCCL all-to-all transpose between passes)" if sharded else
+        "parallelism": ((f"row slabs x{shards} (band solves partitioned across GPUs: slab records all-gathered, "
+                         "halo rows exchanged)" if shard_mode == "slabs" else
+                         f"line-slab shards x{shards} (NCCL all-to-all transpose between passes)") if sharded else
                         ("batch-shard" if wl.sparse else "replicas") + f" x{n}"),
     }
 
@@ -190,10 +196,12 @@ def main():
     # ---- inputs for this rank
     if sharded:
         from paper_1705_01674_b200.sharded import DistExchange, LocalExchange, ShardedSmoother
+        from paper_1705_01674_b200.slabs import SlabSmoother
 
         ht, hg = WL.GENERATORS[wl.name](0)  # ONE image, cut into windows
         ex = DistExchange() if world > 1 else LocalExchange(args.local_shards)
-        sm = ShardedSmoother(wl.height, wl.width, wl.channels, 1, wl.cfg, exchange=ex)
+        Smoother = SlabSmoother if args.shard_mode == "slabs" else ShardedSmoother
+        sm = Smoother(wl.height, wl.width, wl.channels, 1, wl.cfg, exchange=ex)
         sm.load(ht, hg)
         batch_per_rank = 1
         px_step = wl.width * wl.height // world  # whole-image pixels per step, shared by the ranks
@@ -321,7 +329,9 @@ def main():
         "launch_unit": "one directional pass: ka_tile (chunk spike-forward + in-tile reduction; solves the "
                        "reduced system itself when short) [+ k2_tree (super-separator solve)] + kb_tile (interior "
                        "solve + averaging + transposed store); duration = timed step / T"
-                       + ("; sharded: includes the all-to-all transpose" if sharded else ""),
+                       + (("; sharded: includes the slab-record all-gather and halo exchange"
+                           if args.shard_mode == "slabs" else "; sharded: includes the all-to-all transpose")
+                          if sharded else ""),
         "bytes_alg_per_pass": pass_bytes, "pass_ms": pass_ms,
         "dominant_kernel": dominant,
         "dominant_share": (kern[dominant]["ms"] / kern_total) if dominant else None,
@@ -356,7 +366,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "MPix/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f32", "data": DATA,
-            "config": config_block(wl, world, batch_per_rank, sharded, sm.G if sharded else 1),
+            "config": config_block(wl, world, batch_per_rank, sharded, sm.G if sharded else 1, args.shard_mode),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * args.steps,
             "clocks": clocks, "kernels_instrumented": kernels,
             "step_ms_median": statistics.median(step_ms),
@@ -460,7 +470,7 @@ def e2e_sharded(args, wl, sm, ht, hg, world):
         el = float(tt.item())
     return {"value": wl.width * wl.height * args.steps / el / 1e6, "unit": "MPix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": el / args.steps * 1e3,
-            "api": "ShardedSmoother.load_windows + run + owned rows D2H (pinned host buffers)"}
+            "api": f"{type(sm).__name__}.load_windows + run + owned rows D2H (pinned host buffers)"}
 
 
 def reference_arm(args, wl, rank, world):

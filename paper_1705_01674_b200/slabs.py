@@ -107,13 +107,13 @@ class SlabSmoother:
 
         dev, W, Cc, Cg = self.device, self.W, self.C, self.Cg
         f32 = dict(dtype=torch.float32, device=dev)
-        self.buf, self.gslab, self.gwinT, self.tmpT, self.work, self.rec = {}, {}, {}, {}, {}, {}
+        self.buf, self.gwin, self.gwinT, self.tmpT, self.work = {}, {}, {}, {}, {}
         recn = None
         for g in self.ex.local:
             a, b = self.slabs[g]
             w = self.win[g]
             self.buf[g] = [torch.empty((w.width, W, Cc), **f32) for _ in range(2)]  # ping-pong row windows
-            self.gslab[g] = torch.zeros((b - a + 1, W, Cg), **f32)  # row 0 = row a-1 (halo)
+            self.gwin[g] = torch.empty((w.width, W, Cg), **f32)  # guidance rows [s, e)
             self.gwinT[g] = torch.empty((W, w.width, Cg), **f32)
             self.tmpT[g] = torch.empty((W, w.width, Cc), **f32)
             work, recn = self._sizes(b - a)
@@ -140,12 +140,51 @@ class SlabSmoother:
             a, b = self.slabs[g]
             w = self.win[g]
             self.buf[g][0][a - w.s:b - w.s].copy_(t[a:b])
-            if a > 0:
-                self.gslab[g][0].copy_(gd[a - 1])
-            self.gslab[g][1:].copy_(gd[a:b])
-            gwin = gd[w.s:w.e].to(self.device).contiguous()
-            _transpose(gwin, self.gwinT[g])
+            self.gwin[g].copy_(gd[w.s:w.e])
+            _transpose(self.gwin[g], self.gwinT[g])
         self.cur = 0
+
+    def _guid_rows(self, g: int):
+        """Guidance from slab row a on; row a-1 (the previous slab's last) precedes it in memory."""
+        return self.gwin[g][self.slabs[g][0] - self.win[g].s:]
+
+    def host_windows(self, target, guidance) -> dict:
+        """This process's slab rows and guidance window as pinned host tensors (for load_windows)."""
+        import torch
+
+        t = self._hwc(target)
+        gd = self._hwc(guidance)
+        pin = (lambda x: x.contiguous().pin_memory()) if torch.cuda.is_available() else (lambda x: x.contiguous())
+        out = {}
+        for g in self.ex.local:
+            a, b = self.slabs[g]
+            w = self.win[g]
+            out[g] = (pin(t[a:b]), pin(gd[w.s:w.e]))
+        return out
+
+    def load_windows(self, windows: dict) -> None:
+        """Stream-ordered upload of host_windows() output (slab rows + guidance window)."""
+        for g, (x, gw) in windows.items():
+            self._own(g, 0).copy_(x, non_blocking=True)
+            self.gwin[g].copy_(gw, non_blocking=True)
+            _transpose(self.gwin[g], self.gwinT[g])
+        self.cur = 0
+
+    def window_bytes(self) -> int:
+        return sum(4 * (self._own(g, 0).numel() + self.gwin[g].numel()) for g in self.ex.local)
+
+    def kernel_launches(self) -> int:
+        """Native kernels one run() launches in this process."""
+        from .api import kernel_launches
+
+        n = 0
+        for p in range(self.T):
+            for g in self.ex.local:
+                if ((self.fa + p) & 1) == 0:  # KA, slab reduce | slab solve, [KC,] KB
+                    n += 4 + (1 if self.cfg.r >= 2 else 0)
+                else:  # window transpose + one pass
+                    n += 1 + kernel_launches(self.win[g].width, self.W, self.C, self.Cg, 1, False, self.pcfg)
+        return n
 
     # ---------------------------------------------------------------- passes
     def _own(self, g: int, k: int):
@@ -159,7 +198,7 @@ class SlabSmoother:
         for g in self.ex.local:
             a, b = self.slabs[g]
             src = self._own(g, self.cur)
-            guid = self.gslab[g][1:]
+            guid = self._guid_rows(g)
             st = C.c_void_p(self._stream(g))
             N.check(N.lib().sgwls_b200_slab_pass_a(src.data_ptr(), guid.data_ptr(), self.W, b - a, self.C, self.Cg,
                                                    a, self.G, g, C.byref(self.nc), self.work[g].data_ptr(),
@@ -168,7 +207,7 @@ class SlabSmoother:
         for g in self.ex.local:
             a, b = self.slabs[g]
             src = self._own(g, self.cur)
-            guid = self.gslab[g][1:]
+            guid = self._guid_rows(g)
             out = self._own(g, nxt)
             st = C.c_void_p(self._stream(g))
             N.check(N.lib().sgwls_b200_slab_pass_b(src.data_ptr(), guid.data_ptr(), self.W, b - a, self.C, self.Cg,
