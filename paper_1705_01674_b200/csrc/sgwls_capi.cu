@@ -615,7 +615,7 @@ int guarded(char* err, size_t errlen, F&& f) {
 // (sgwls_tile.cuh "row-slab mode", sharded.py).
 struct SlabLayout {
     AxisPlan ap;
-    size_t crec = 0, srec = 0, rsc = 0, zext = 0, sepext = 0, zg = 0, bsg = 0, total = 0, record = 0;
+    size_t crec = 0, srec = 0, rsc = 0, zext = 0, sepext = 0, zg = 0, bsg = 0, grec = 0, total = 0, record = 0;
 };
 
 SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_config* cfg, int nslabs) {
@@ -640,6 +640,7 @@ SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_conf
     L.sepext = take((P + 1) * r * C * NL);
     L.zg = take(G * r * C * NL);
     L.bsg = take(G * r * RS * NL);
+    L.grec = take((size_t)kSlabWarps * REC * NL);
     L.total = off;
     L.record = REC * NL;
     return L;
@@ -686,6 +687,7 @@ PassLaunch slab_launch(const SlabLayout& L, const float* src, const float* guid,
     pl.sep = work + L.sepext + rC * NL;  // one slot in front: sep[-1]
     pl.zg = work + L.zg;
     pl.bsg = work + L.bsg;
+    pl.grec = work + L.grec;
     pl.nslab = nslabs;
     pl.islab = islab;
     pl.transpose_out = 0;

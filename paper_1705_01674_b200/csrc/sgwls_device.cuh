@@ -107,6 +107,8 @@ __host__ __device__ constexpr bool tile_fuse_k2(int PS) { return PS > 1 && PS <=
 // group solves that group's reduced system (depth ~2*PS/NW + NW) and raises a
 // flag; KB tiles wait on their own groups' flags only.
 constexpr int kFlagMaxSuper = 64;
+// warps per band group of the row-slab reduce / solve kernels (sgwls_tile.cuh)
+constexpr int kSlabWarps = 16;
 
 __device__ __forceinline__ float fast_ex2(float x) {
     float y;

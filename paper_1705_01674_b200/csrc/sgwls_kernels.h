@@ -46,6 +46,7 @@ struct PassLaunch {
     int nslab = 1, islab = 0;
     float* zg = nullptr;   // nslab-1 slab separators
     float* bsg = nullptr;  // their back-substitution rows
+    float* grec = nullptr; // group records of the slab (phase A -> B), kSlabWarps x REC per band
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);

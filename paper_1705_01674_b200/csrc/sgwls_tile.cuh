@@ -1075,55 +1075,118 @@ __host__ inline size_t kc_smem(int NWA, int nty) {
 // slab, G is tiny), then the slab's own super-separators with its two slab
 // separators as boundary values; then KC / KB as usual.  Only slab records
 // cross GPUs -- never image data.
+// Both slab kernels run one CTA of NG warps per group of 32 bands (lane = band),
+// with the tree of k2_tree_body: warp w owns a contiguous group of the slab's
+// super-records, so the serial depth is ~PS/NG + NG instead of PS.
+//
+// Phase A: level 1, warp w reduces its group to a group record (kept in
+// grec[w][field][line] for phase B); level 2, warp 0 reduces the group records
+// to the slab record.
 template <int R, int C>
-__global__ void __launch_bounds__(128) k2_slab_reduce(const PassGeom g, int PS, const float* __restrict__ srec,
-                                                      float* __restrict__ slabrec) {
+__global__ void __launch_bounds__(512) k2_slab_reduce(const PassGeom g, int PS, const float* __restrict__ srec,
+                                                      float* __restrict__ grec, float* __restrict__ slabrec) {
     using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, w = threadIdx.y, NG = blockDim.y;
     const int NL = g.nb * g.batch;
     const long long NLl = NL;
-    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    const int L = blockIdx.x * 32 + lane;
+    const bool ok = L < NL;
+    const int NGa = min(NG, PS);
+    const int J0 = (int)((long long)w * PS / NGa), J1 = (int)((long long)(w + 1) * PS / NGa);
+    const int rsG = NG * 32 + 1;
     pdl_wait();  // KA's super-records
     pdl_trigger();
-    if (L >= NL) return;
-    reduce_super<R, C>(srec + L, NLl, (long long)RL::REC * NLl, PS, !g.has_prev, !g.has_next, slabrec + L, NLl);
+    if (w < NGa && ok) {
+        float* gout = sm + w * 32 + lane;
+        reduce_super<R, C>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0,
+                           w == 0 && !g.has_prev, w == NGa - 1 && !g.has_next, gout, rsG);
+#pragma unroll 1
+        for (int f = 0; f < RL::REC; ++f) grec[((long long)w * RL::REC + f) * NLl + L] = gout[f * rsG];
+    }
+    __syncthreads();
+    if (w == 0 && ok)
+        reduce_super<R, C>(sm + lane, rsG, 32, NGa, !g.has_prev, !g.has_next, slabrec + L, NLl);
 }
 
-// allrec: the G slab records [slab][field][line]; z: this slab's super-separator
-// array with one slot in front (z[-1] = the previous slab's separator, z[PS-1]
-// = this slab's last separator); zg / bsg: global separators / back-substitution
-// scratch; rsc: local back-substitution scratch.
+// Phase B: warp 0 solves the G-1 slab separators (allrec, the same tiny system
+// on every slab), then the group-level system of this slab with its two slab
+// separators as boundary values (level 2); every warp then solves its group's
+// super-separators (level 3).  z carries one slot in front: z[-1] = the
+// previous slab's separator, z[PS-1] = this slab's last separator.
 template <int R, int C>
-__global__ void __launch_bounds__(128) k2_slab_solve(const PassGeom g, int PS, int G, int gi,
+__global__ void __launch_bounds__(512) k2_slab_solve(const PassGeom g, int PS, int G, int gi,
                                                      const float* __restrict__ allrec, const float* __restrict__ srec,
-                                                     float* __restrict__ zg, float* __restrict__ bsg,
-                                                     float* __restrict__ rsc, float* __restrict__ z) {
+                                                     const float* __restrict__ grec, float* __restrict__ zg,
+                                                     float* __restrict__ bsg, float* __restrict__ rsc,
+                                                     float* __restrict__ z) {
     using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, w = threadIdx.y, NG = blockDim.y;
     const int NL = g.nb * g.batch;
     const long long NLl = NL;
-    const int L = blockIdx.x * blockDim.x + threadIdx.x;
+    const int L = blockIdx.x * 32 + lane;
+    const bool ok = L < NL;
+    const int NGa = min(NG, PS);
+    const int J0 = (int)((long long)w * PS / NGa), J1 = (int)((long long)(w + 1) * PS / NGa);
+    float* zgrp = sm;                         // (NG + 1) x R*C x 32: [0] = zL, [k+1] = group k's separator
+    float* bs2 = zgrp + (NG + 1) * R * C * 32;  // NG x R x RS x 32
     pdl_wait();
     pdl_trigger();
-    if (L >= NL) return;
-    float z0[R][C], zL[R][C], zR[R][C];
+    if (w == 0 && ok) {
+        float z0[R][C], zL[R][C], zR[R][C];
 #pragma unroll
-    for (int q = 0; q < R; ++q)
+        for (int q = 0; q < R; ++q)
 #pragma unroll
-        for (int c = 0; c < C; ++c) z0[q][c] = 0.f;
-    // the G-1 slab separators (every slab solves the same tiny system)
-    if (G > 1)
-        solve_inner<R, C>(allrec + L, NLl, (long long)RL::REC * NLl, G, false, z0, false, z0, zg + L, NLl, bsg + L,
-                          NLl);
+            for (int c = 0; c < C; ++c) z0[q][c] = 0.f;
+        if (G > 1)
+            solve_inner<R, C>(allrec + L, NLl, (long long)RL::REC * NLl, G, false, z0, false, z0, zg + L, NLl,
+                              bsg + L, NLl);
 #pragma unroll
-    for (int q = 0; q < R; ++q)
+        for (int q = 0; q < R; ++q)
 #pragma unroll
-        for (int c = 0; c < C; ++c) {
-            zL[q][c] = g.has_prev ? zg[((long long)((gi - 1) * R + q) * C + c) * NLl + L] : 0.f;
-            zR[q][c] = g.has_next ? zg[((long long)(gi * R + q) * C + c) * NLl + L] : 0.f;
-            if (g.has_prev) z[((long long)(-R + q) * C + c) * NLl + L] = zL[q][c];
-            if (g.has_next) z[((long long)((PS - 1) * R + q) * C + c) * NLl + L] = zR[q][c];
+            for (int c = 0; c < C; ++c) {
+                zL[q][c] = g.has_prev ? zg[((long long)((gi - 1) * R + q) * C + c) * NLl + L] : 0.f;
+                zR[q][c] = g.has_next ? zg[((long long)(gi * R + q) * C + c) * NLl + L] : 0.f;
+                zgrp[(q * C + c) * 32 + lane] = zL[q][c];
+                if (g.has_prev) z[((long long)(-R + q) * C + c) * NLl + L] = zL[q][c];
+                zgrp[((NGa * R + q) * C + c) * 32 + lane] = zR[q][c];  // slot of the last group's separator
+            }
+        if (NGa > 1)
+            solve_inner<R, C>(grec + L, NLl, (long long)RL::REC * NLl, NGa, g.has_prev, zL, g.has_next, zR,
+                              zgrp + R * C * 32 + lane, 32, bs2 + lane, 32);
+    }
+    __syncthreads();
+    if (w < NGa && ok) {
+        const bool has_l = w > 0 || g.has_prev, has_r = w < NGa - 1 || g.has_next;
+        float zL[R][C], zR[R][C];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                zL[q][c] = zgrp[((w * R + q) * C + c) * 32 + lane];
+                zR[q][c] = zgrp[(((w + 1) * R + q) * C + c) * 32 + lane];
+            }
+        if (has_r) {  // the group's last super-separator (stored before the solve, see kb_tile step 2)
+            float* zo = z + (long long)(J1 - 1) * R * C * NLl + L;
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-    solve_inner<R, C>(srec + L, NLl, (long long)RL::REC * NLl, PS, g.has_prev, zL, g.has_next, zR, z + L, NLl,
-                      rsc + L, NLl);
+        solve_inner<R, C>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0, has_l, zL,
+                          has_r, zR, z + (long long)J0 * R * C * NLl + L, NLl,
+                          rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
+    }
+}
+
+template <int R, int C>
+__host__ inline size_t k2_slab_reduce_smem(int NG) {
+    return (size_t)Rec<R, C>::REC * (NG * 32 + 1) * sizeof(float);
+}
+template <int R, int C>
+__host__ inline size_t k2_slab_solve_smem(int NG) {
+    return ((size_t)(NG + 1) * R * C * 32 + (size_t)NG * R * Rec<R, C>::RS * 32) * sizeof(float);
 }
 
 // ===================================================================== KB
@@ -1467,15 +1530,22 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             if (e != cudaSuccess) return e;
         }
         ProfScope ps("k2_slab_reduce", st);
-        e = launch_pdl(k2_slab_reduce<R, C>, dim3((NL + 127) / 128), dim3(128), 0, st, g, PSA, (const float*)pl.rec,
-                       pl.slabrec);
+        const size_t sm2 = k2_slab_reduce_smem<R, C>(kSlabWarps);
+        e = cudaFuncSetAttribute(k2_slab_reduce<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(k2_slab_reduce<R, C>, dim3((NL + 31) / 32), dim3(32, kSlabWarps), sm2, st, g, PSA,
+                       (const float*)pl.rec, pl.grec, pl.slabrec);
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
     if (pl.slab_phase == 2) {  // row-slab phase B: separators, then KC / KB below
         ProfScope ps("k2_slab_solve", st);
-        e = launch_pdl(k2_slab_solve<R, C>, dim3((NL + 127) / 128), dim3(128), 0, st, g, PSA, pl.nslab, pl.islab,
-                       (const float*)pl.slabrec, (const float*)pl.rec, pl.zg, pl.bsg, pl.rs, pl.z);
+        const size_t sm2 = k2_slab_solve_smem<R, C>(kSlabWarps);
+        e = cudaFuncSetAttribute(k2_slab_solve<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(k2_slab_solve<R, C>, dim3((NL + 31) / 32), dim3(32, kSlabWarps), sm2, st, g, PSA, pl.nslab,
+                       pl.islab, (const float*)pl.slabrec, (const float*)pl.rec, (const float*)pl.grec, pl.zg, pl.bsg,
+                       pl.rs, pl.z);
         if (e != cudaSuccess) return e;
     }
     if (g.P > 1 && !slab) {

@@ -223,7 +223,7 @@ class SlabSmoother:
         for g in self.ex.local:
             _transpose(self.buf[g][self.cur], self.tmpT[g])
             # Column pass on the transposed window, written transposed: rows [s, e) of the image
-            pass_device(self.tmpT[g], self.gwinT[g], self.pcfg, out=self.buf[g][nxt])
+            pass_device(self.tmpT[g], self.gwinT[g], self.pcfg, out=self.buf[g][nxt], graph=True)
         self.cur = nxt
 
     def _stream(self, g: int) -> int:
