@@ -314,14 +314,26 @@ def main():
     kern = {k: v for k, v in prof.items() if k != "pass"}
     dominant = max(kern, key=lambda k: kern[k]["ms"]) if kern else None
     kern_total = sum(v["ms"] for v in kern.values()) or 1.0
-    traffic = None
+    traffic, winst = None, None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{wl.name}.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and not sharded:
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get("dram_bytes_per_pass")
+                tj = json.load(f)
+            traffic, winst = tj.get("dram_bytes_per_pass"), tj.get("warp_inst_per_pass")
         except Exception:
-            traffic = None
+            traffic = winst = None
+    # the kernels are bound by instruction issue, not HBM: executed warp
+    # instructions of one pass (ncu, profiles/) / the live pass time, against
+    # 4 issue slots per SM per cycle at the sampled SM clock
+    issue = None
+    if winst:
+        nsm = torch.cuda.get_device_properties(local).multi_processor_count
+        clk = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        ipeak = nsm * 4 * clk
+        iach = winst / (pass_ms / 1e3)
+        issue = {"unit": "warp-instr/s", "achieved": iach, "peak": ipeak, "frac": iach / ipeak,
+                 "warp_inst_per_pass": winst, "source": "ncu smsp__inst_executed.sum per pass (profiles/)"}
     filter_bytes = wl.bytes_alg() * batch_per_rank // wl.batch // (world if sharded else 1)
     roofline = {
         "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
@@ -338,6 +350,7 @@ def main():
         "filter_bytes_alg": filter_bytes,
         "filter_frac": filter_bytes / (total_ms / args.steps / 1e3) / 1e9 / peak,
         "frac_vs_8tbs_nameplate": achieved / 8000.0,
+        "issue": issue,
     }
     kernels = {k: {"launches_per_step": v["launches"] / psteps, "ms_per_step_instrumented": v["ms"] / psteps,
                    "share": v["ms"] / kern_total} for k, v in kern.items()}
