@@ -989,6 +989,10 @@ struct TileOut {
     int jfast;         // grid order (chunk tile fastest)
 };
 
+// 1/n correctly rounded (what 1.0f / n gives) for the band count of a column, n <= 2r + 2 <= 10
+__constant__ float kInvCount[12] = {0.f, 1.f / 1, 1.f / 2, 1.f / 3, 1.f / 4, 1.f / 5, 1.f / 6,
+                                    1.f / 7, 1.f / 8, 1.f / 9, 1.f / 10, 1.f / 11};
+
 __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, int& bmax) {
     const int r = g.r, tau = g.tau;
     const int lo_b = x - 2 * r;
@@ -1365,14 +1369,32 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         // owner CTA = ceil((bmax - 31) / step) (0 if bmax <= 31), tested without a division
         const int bx = bxi, q = bmax - 31;
         const bool owned = bx == 0 ? q <= 0 : (q > (bx - 1) * to.step && q <= bx * to.step);
-        const float inv = 1.0f / (float)(bmax - bmin + 1);
+        const float inv = kInvCount[bmax - bmin + 1];  // == 1.0f / count, without the IEEE-division slow path
         inv_col[xl] = owned ? inv : -inv;
+#ifndef SGWLS_ZERO_ALL
+        if (to.nph == 2) {
+            // phase 0 STORES (step 4), so only the columns no phase-0 band of this
+            // tile covers start from zero (measured: c5 +1.2 %, c4 +0.7 %; with
+            // more phases the sparse phase-0 coverage makes it a loss, c3 -6 %)
+            bool cov0 = false;
+            for (int bb = bmin; bb <= bmax; ++bb) {
+                const int l = bb - B0;
+                cov0 = cov0 || (l >= 0 && l < 32 && bb < g.nb && (l % to.nph) == 0);
+            }
+            if (!cov0)
+                for (int y = 0; y < TR; ++y)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) tl[xl * sx + y * sy + c] = 0.f;
+        }
+#endif
     }
-    if (to.nph > 1) {
-        if (colmaj)
-            for (int i = tid; i < tsize / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        else  // (the tile region is padded to a multiple of 4 floats)
-            for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+#ifdef SGWLS_ZERO_ALL  // A/B: zero the whole tile, every phase accumulates
+    const bool store_first = false;
+#else
+    const bool store_first = to.nph == 2;
+#endif
+    if (to.nph > 1 && !store_first) {
+        for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
     // chunk factor state in registers: couplings cs[p][i] and y / u values ys[p][c]
@@ -1409,7 +1431,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                     const bool rev = (par0 ^ (rr & 1)) != 0;
                     float* tp = tbase + (rev ? oo : oe);
                     const float sc = rev ? csc[M - 1 - jj] : csc[jj];
-                    if (to.nph == 1) {
+                    if (to.nph == 1 || (store_first && ph == 0)) {  // first writer of every cell it touches
 #pragma unroll
                         for (int c = 0; c < C; ++c) tp[c] = ys[p][c] * sc;
                     } else {
