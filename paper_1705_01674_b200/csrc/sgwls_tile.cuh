@@ -977,6 +977,56 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
 
 // ===================================================================== KB
 
+// Averaging of one chunk's rows into the output tile by warp shuffles, for a
+// tile whose 32 bands all sit on the tau grid (band lane l covers local columns
+// [TAU*l, TAU*l + M)).  Lane l owns columns [TAU*l, TAU*l + TAU): it receives
+// the overlapping values of lanes l-1, l-2, ... (__shfl_up), sums them in
+// increasing band order like the reference (proj/src/smoother.cpp:78-90),
+// scales by 1/count and stores each tile cell exactly once -- no zeroing, no
+// phase loop, no shared-memory read-modify-write.  Lanes past the last band
+// (ys = 0) still take part, so the image's last columns get their sums.
+// Columns whose covering bands start before lane 0 come out partial; they are
+// never owned by this tile unless the tile starts the image, where those bands
+// do not exist.
+template <int TAU, int R, int C, int K>
+__device__ __forceinline__ void average_shfl(const float (&ys)[K][C], int nrw, int par0, int lane, float* trow,
+                                             int sx, int sy, int ncol, const float* inv_col) {
+    constexpr int M = 2 * R + 1;
+    constexpr int KMAX = (M - 1) / TAU;  // lanes back whose bands reach this lane's columns
+#pragma unroll
+    for (int rr = 0; rr < K / M; ++rr) {
+        if (rr < nrw) {
+            const bool rev = (par0 ^ (rr & 1)) != 0;
+#pragma unroll
+            for (int j = 0; j < TAU; ++j) {
+                const int xl = TAU * lane + j;
+                float acc[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) acc[c] = 0.f;
+#pragma unroll
+                for (int k = KMAX; k >= 1; --k) {
+                    if (j + k * TAU < M) {
+                        const int m = j + k * TAU;
+#pragma unroll
+                        for (int c = 0; c < C; ++c) {
+                            const float v = rev ? ys[rr * M + (M - 1 - m)][c] : ys[rr * M + m][c];
+                            const float u = __shfl_up_sync(0xffffffffu, v, k);
+                            if (lane >= k) acc[c] += u;  // no band before lane 0 (image start)
+                        }
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < C; ++c) acc[c] += rev ? ys[rr * M + (M - 1 - j)][c] : ys[rr * M + j][c];
+                if (xl < ncol) {
+                    const float sc = fabsf(inv_col[xl]);
+#pragma unroll
+                    for (int c = 0; c < C; ++c) trow[xl * sx + rr * sy + c] = acc[c] * sc;
+                }
+            }
+        }
+    }
+}
+
 struct TileOut {
     float* out;
     int transpose_out;
@@ -1360,6 +1410,15 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     }
     const int kv = nrows * M;
     const int kend = lastc ? kv : kv - R;  // interior positions [0, kend)
+    // Shuffle averaging (average_shfl) when the bands overlap, all bands of the
+    // tile are on the tau grid, tau <= 3, and the last owned column has a writer lane
+    const bool last_cta = B0 + 32 >= g.nb;
+#ifndef SGWLS_NO_SHFL_AVG
+    const bool shfl_avg = to.nph > 1 && g.tau <= 3 && bl < g.nreg &&
+                          (!last_cta || (bl - B0) + (M - 1) / g.tau <= 31);
+#else
+    const bool shfl_avg = false;
+#endif
     // per-column averaging scale 1/count, positive if this CTA owns the column
     // (writes it out), negative otherwise
     float* inv_col = tl + ((tsize + 3) & ~3);
@@ -1372,7 +1431,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         const float inv = kInvCount[bmax - bmin + 1];  // == 1.0f / count, without the IEEE-division slow path
         inv_col[xl] = owned ? inv : -inv;
 #ifndef SGWLS_ZERO_ALL
-        if (to.nph == 2) {
+        if (to.nph == 2 && !shfl_avg) {
             // phase 0 STORES (step 4), so only the columns no phase-0 band of this
             // tile covers start from zero (measured: c5 +1.2 %, c4 +0.7 %; with
             // more phases the sparse phase-0 coverage makes it a loss, c3 -6 %)
@@ -1393,7 +1452,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
 #else
     const bool store_first = to.nph == 2;
 #endif
-    if (to.nph > 1 && !store_first) {
+    if (to.nph > 1 && !store_first && !shfl_avg) {
         for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
 
@@ -1421,7 +1480,18 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     float csc[M];
 #pragma unroll
     for (int jj = 0; jj < M; ++jj) csc[jj] = active ? fabsf(inv_col[lo - xa + jj]) : 0.f;
-    for (int ph = 0; ph < to.nph; ++ph) {
+    if (shfl_avg) {
+        const int nrw = wid < nw ? min(RW, g.Hl - y0) : 0;  // rows of this warp's chunk (all lanes)
+        float* trow = tl + (y0 - Y0) * sy;
+        switch (g.tau) {
+            case 1: average_shfl<1, R, C, K>(ys, nrw, par0, lane, trow, sx, sy, ncol, inv_col); break;
+            case 2: average_shfl<2, R, C, K>(ys, nrw, par0, lane, trow, sx, sy, ncol, inv_col); break;
+            default: average_shfl<3, R, C, K>(ys, nrw, par0, lane, trow, sx, sy, ncol, inv_col); break;
+        }
+        fence_proxy_async_shared();
+        __syncthreads();
+    }
+    for (int ph = 0; ph < (shfl_avg ? 0 : to.nph); ++ph) {
         if (active && (lane % to.nph) == ph) {
 #pragma unroll
             for (int p = 0; p < K; ++p) {
