@@ -1027,6 +1027,66 @@ __device__ __forceinline__ void average_shfl(const float (&ys)[K][C], int nrw, i
     }
 }
 
+// Same averaging, stored straight to the next pass's (transposed) layout instead
+// of the shared output tile: lane l's column x = xa + TAU*l + j is output row x,
+// and this chunk's RW rows are RW*C consecutive floats of it (vector stores of
+// VEC floats; the last, short chunk stores scalars).  Only owned columns.
+template <int TAU, int R, int C, int K, int VEC>
+__device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int nrw, int par0, int lane,
+                                                    float* obase, long long opitch, int ncol,
+                                                    const float* inv_col) {
+    constexpr int M = 2 * R + 1, RW = K / M;
+    constexpr int KMAX = (M - 1) / TAU;
+    float acc[TAU][RW * C];
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+        const bool rev = (par0 ^ (rr & 1)) != 0;
+#pragma unroll
+        for (int j = 0; j < TAU; ++j) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[j][rr * C + c] = 0.f;
+#pragma unroll
+            for (int k = KMAX; k >= 1; --k) {
+                if (j + k * TAU < M) {
+                    const int m = j + k * TAU;
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        const float v = rev ? ys[rr * M + (M - 1 - m)][c] : ys[rr * M + m][c];
+                        const float u = __shfl_up_sync(0xffffffffu, v, k);
+                        if (lane >= k) acc[j][rr * C + c] += u;
+                    }
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc[j][rr * C + c] += rev ? ys[rr * M + (M - 1 - j)][c] : ys[rr * M + j][c];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < TAU; ++j) {
+        const int xl = TAU * lane + j;
+        if (xl >= ncol) continue;
+        const float sc = inv_col[xl];
+        if (!(sc > 0.f)) continue;  // not owned by this tile
+        float* op = obase + (long long)xl * opitch;
+        if (nrw == RW) {
+#pragma unroll
+            for (int e = 0; e < RW * C; e += VEC) {
+                if constexpr (VEC == 4)
+                    *reinterpret_cast<float4*>(op + e) =
+                        make_float4(acc[j][e] * sc, acc[j][e + 1] * sc, acc[j][e + 2] * sc, acc[j][e + 3] * sc);
+                else if constexpr (VEC == 2)
+                    *reinterpret_cast<float2*>(op + e) = make_float2(acc[j][e] * sc, acc[j][e + 1] * sc);
+                else
+                    op[e] = acc[j][e] * sc;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < RW * C; ++e)
+                if (e < nrw * C) op[e] = acc[j][e] * sc;
+        }
+    }
+}
+
 struct TileOut {
     float* out;
     int transpose_out;
@@ -1480,6 +1540,31 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     float csc[M];
 #pragma unroll
     for (int jj = 0; jj < M; ++jj) csc[jj] = active ? fabsf(inv_col[lo - xa + jj]) : 0.f;
+    // direct stores to the transposed output (no tile round trip) when the
+    // vector width divides the output rows
+    constexpr int DVEC = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
+#ifndef SGWLS_NO_DIRECT
+    // measured on B200: c1 +8.5 %, c3 +1.8 %, c5 +0.6 %; c4 (2 channels, float2 runs) -4.7 %, so
+    // only for one channel or full float4 runs
+    const bool direct = shfl_avg && to.transpose_out && (C == 1 || DVEC == 4) && ((long long)g.Hl * C) % DVEC == 0 &&
+                        (reinterpret_cast<uintptr_t>(oi) & (DVEC * 4 - 1)) == 0;
+#else
+    const bool direct = false;
+#endif
+    if (direct) {
+        const int nrw = wid < nw ? min(RW, g.Hl - y0) : 0;
+        float* obase = oi + ((long long)xa * g.Hl + y0) * C;
+        const long long opitch = (long long)g.Hl * C;
+        if (nrw > 0) {
+            switch (g.tau) {
+                case 1: average_shfl_direct<1, R, C, K, DVEC>(ys, nrw, par0, lane, obase, opitch, ncol, inv_col); break;
+                case 2: average_shfl_direct<2, R, C, K, DVEC>(ys, nrw, par0, lane, obase, opitch, ncol, inv_col); break;
+                default: average_shfl_direct<3, R, C, K, DVEC>(ys, nrw, par0, lane, obase, opitch, ncol, inv_col); break;
+            }
+        }
+        if (flagged) pdl_wait();
+        return;
+    }
     if (shfl_avg) {
         const int nrw = wid < nw ? min(RW, g.Hl - y0) : 0;  // rows of this warp's chunk (all lanes)
         float* trow = tl + (y0 - Y0) * sy;
