@@ -817,7 +817,9 @@ template <int R, int C, int CG>
 #endif
 #define SGWLS_KA_BOUNDS __launch_bounds__(256, SGWLS_KA_MINB)
 #ifndef SGWLS_KB_MINB_KC
-#define SGWLS_KB_MINB_KC 3  // KB after KC: <= 85 registers (measured +3% c5, +8% c4)
+// KB after KC: <= 85 registers (measured +3% c5, +8% c4); <= 64 for one channel
+// once the averaging went to shuffles and direct stores (c5 +1.6 %, c3 +0.7 %; c4 -1 %)
+#define SGWLS_KB_MINB_KC (C == 1 ? 4 : 3)
 #endif
 // the INNER variant (r = 1) spills badly under a tighter budget: 2 CTAs (<= 128)
 #define SGWLS_KB_BOUNDS __launch_bounds__(256, (INNER ? 2 : SGWLS_KB_MINB_KC))
@@ -1383,6 +1385,53 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     // grid that may still be running).
     const bool flagged = INNER && multi && to.flags != nullptr;
     const bool early = flagged || (multi && (!INNER || to.early_rec));
+    // ---- 0. tile geometry (column ownership, 1/count, zeroing): independent of the
+    //         predecessor, so it runs before the dependent-launch wait
+    // Shuffle averaging (average_shfl) when the bands overlap, all bands of the
+    // tile are on the tau grid, tau <= 3, and the last owned column has a writer lane
+    const bool last_cta = B0 + 32 >= g.nb;
+#ifndef SGWLS_NO_SHFL_AVG
+    const bool shfl_avg = to.nph > 1 && g.tau <= 3 && bl < g.nreg &&
+                          (!last_cta || (bl - B0) + (M - 1) / g.tau <= 31);
+#else
+    const bool shfl_avg = false;
+#endif
+    // per-column averaging scale 1/count, positive if this CTA owns the column
+    // (writes it out), negative otherwise
+    float* inv_col = tl + ((tsize + 3) & ~3);
+    for (int xl = tid; xl < ncol; xl += NT) {
+        int bmin, bmax;
+        covering(g, xa + xl, bmin, bmax);
+        // owner CTA = ceil((bmax - 31) / step) (0 if bmax <= 31), tested without a division
+        const int bx = bxi, q = bmax - 31;
+        const bool owned = bx == 0 ? q <= 0 : (q > (bx - 1) * to.step && q <= bx * to.step);
+        const float inv = kInvCount[bmax - bmin + 1];  // == 1.0f / count, without the IEEE-division slow path
+        inv_col[xl] = owned ? inv : -inv;
+#ifndef SGWLS_ZERO_ALL
+        if (to.nph == 2 && !shfl_avg) {
+            // phase 0 STORES (step 4), so only the columns no phase-0 band of this
+            // tile covers start from zero (measured: c5 +1.2 %, c4 +0.7 %; with
+            // more phases the sparse phase-0 coverage makes it a loss, c3 -6 %)
+            bool cov0 = false;
+            for (int bb = bmin; bb <= bmax; ++bb) {
+                const int l = bb - B0;
+                cov0 = cov0 || (l >= 0 && l < 32 && bb < g.nb && (l % to.nph) == 0);
+            }
+            if (!cov0)
+                for (int y = 0; y < TR; ++y)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) tl[xl * sx + y * sy + c] = 0.f;
+        }
+#endif
+    }
+#ifdef SGWLS_ZERO_ALL  // A/B: zero the whole tile, every phase accumulates
+    const bool store_first = false;
+#else
+    const bool store_first = to.nph == 2;
+#endif
+    if (to.nph > 1 && !store_first && !shfl_avg) {
+        for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     if (!early) pdl_wait();
     if (active)
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
@@ -1470,51 +1519,6 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     }
     const int kv = nrows * M;
     const int kend = lastc ? kv : kv - R;  // interior positions [0, kend)
-    // Shuffle averaging (average_shfl) when the bands overlap, all bands of the
-    // tile are on the tau grid, tau <= 3, and the last owned column has a writer lane
-    const bool last_cta = B0 + 32 >= g.nb;
-#ifndef SGWLS_NO_SHFL_AVG
-    const bool shfl_avg = to.nph > 1 && g.tau <= 3 && bl < g.nreg &&
-                          (!last_cta || (bl - B0) + (M - 1) / g.tau <= 31);
-#else
-    const bool shfl_avg = false;
-#endif
-    // per-column averaging scale 1/count, positive if this CTA owns the column
-    // (writes it out), negative otherwise
-    float* inv_col = tl + ((tsize + 3) & ~3);
-    for (int xl = tid; xl < ncol; xl += NT) {
-        int bmin, bmax;
-        covering(g, xa + xl, bmin, bmax);
-        // owner CTA = ceil((bmax - 31) / step) (0 if bmax <= 31), tested without a division
-        const int bx = bxi, q = bmax - 31;
-        const bool owned = bx == 0 ? q <= 0 : (q > (bx - 1) * to.step && q <= bx * to.step);
-        const float inv = kInvCount[bmax - bmin + 1];  // == 1.0f / count, without the IEEE-division slow path
-        inv_col[xl] = owned ? inv : -inv;
-#ifndef SGWLS_ZERO_ALL
-        if (to.nph == 2 && !shfl_avg) {
-            // phase 0 STORES (step 4), so only the columns no phase-0 band of this
-            // tile covers start from zero (measured: c5 +1.2 %, c4 +0.7 %; with
-            // more phases the sparse phase-0 coverage makes it a loss, c3 -6 %)
-            bool cov0 = false;
-            for (int bb = bmin; bb <= bmax; ++bb) {
-                const int l = bb - B0;
-                cov0 = cov0 || (l >= 0 && l < 32 && bb < g.nb && (l % to.nph) == 0);
-            }
-            if (!cov0)
-                for (int y = 0; y < TR; ++y)
-#pragma unroll
-                    for (int c = 0; c < C; ++c) tl[xl * sx + y * sy + c] = 0.f;
-        }
-#endif
-    }
-#ifdef SGWLS_ZERO_ALL  // A/B: zero the whole tile, every phase accumulates
-    const bool store_first = false;
-#else
-    const bool store_first = to.nph == 2;
-#endif
-    if (to.nph > 1 && !store_first && !shfl_avg) {
-        for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
 
     // chunk factor state in registers: couplings cs[p][i] and y / u values ys[p][c]
     float cs[K][R], ys[K][C];
@@ -1537,9 +1541,6 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     //         Values enter the tile already divided by their column's count.
     const int par0 = y0 & 1;
     float* tbase = tl + (lo - xa) * sx + (y0 - Y0) * sy;
-    float csc[M];
-#pragma unroll
-    for (int jj = 0; jj < M; ++jj) csc[jj] = active ? fabsf(inv_col[lo - xa + jj]) : 0.f;
     // direct stores to the transposed output (no tile round trip) when the
     // vector width divides the output rows
     constexpr int DVEC = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
@@ -1576,6 +1577,9 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         fence_proxy_async_shared();
         __syncthreads();
     }
+    float csc[M];
+#pragma unroll
+    for (int jj = 0; jj < M; ++jj) csc[jj] = (active && !shfl_avg) ? fabsf(inv_col[lo - xa + jj]) : 0.f;
     for (int ph = 0; ph < (shfl_avg ? 0 : to.nph); ++ph) {
         if (active && (lane % to.nph) == ph) {
 #pragma unroll
