@@ -8,6 +8,7 @@ import subprocess
 import sys
 
 rep, cfg = sys.argv[1], sys.argv[2]
+outp = sys.argv[3] if len(sys.argv) > 3 else f"profiles/ncu_traffic_{cfg}.json"
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
@@ -32,5 +33,5 @@ for r in rows[2:]:
 res = {"config": cfg, "report": rep, "dram_bytes_per_pass": total, "per_kernel": per,
        "warp_inst_per_pass": inst, "warp_inst_per_kernel": inst_per,
        "note": "ncu --set full, one launch of each pass kernel (cold L2 between replays)"}
-json.dump(res, open(f"profiles/ncu_traffic_{cfg}.json", "w"), indent=1)
+json.dump(res, open(outp, "w"), indent=1)
 print(json.dumps(res, indent=1))
