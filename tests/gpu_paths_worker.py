@@ -18,6 +18,12 @@ CASES = [  # (h, w, c, r, tau, lam, T)
     (181, 99, 1, 3, 2, 900.0, 2),
     (140, 77, 1, 4, 5, 100.0, 2),
     (100, 68, 1, 1, 2, 400.0, 2),  # W, H multiples of 4, not of 32: vectorised transpose with edge tiles
+    # shuffle averaging edge cases: a last tile of exactly 32 bands whose tail
+    # columns have no writer lane (falls back to the phase path), a forced last
+    # band centre off the tau grid, two channels
+    (70, 64, 1, 1, 1, 900.0, 1),
+    (90, 100, 1, 1, 2, 400.0, 2),
+    (60, 100, 2, 2, 3, 400.0, 2),
     # tall lines: long reduced systems
     (4100, 40, 2, 1, 2, 400.0, 2),
     (9000, 36, 1, 1, 1, 900.0, 1),
