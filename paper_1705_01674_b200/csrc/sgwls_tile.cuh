@@ -384,12 +384,13 @@ struct Win {
 template <int R, int C, int CG, int RW, bool FULL>
 __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
                                                          bool last, int kv, float* rec, int rs, float* grec,
-                                                         long long gs) {
+                                                         int gs) {
     using RL = Rec<R, C>;
-    // every record field goes to `rec` (shared) and, if given, to `grec` (global)
+    // every record field goes to `rec` (shared) and to `grec` (global; 32-bit field
+    // stride, so each field address is one IMAD.WIDE)
     auto put = [&](int f, float v) {
         rec[f * rs] = v;
-        if (grec != nullptr) grec[f * gs] = v;
+        grec[f * gs] = v;
     };
     constexpr int K = RW * (2 * R + 1);
     Win<R, C, true> w;
@@ -447,8 +448,7 @@ __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG,
 
 template <int R, int C, int CG, int RW>
 __device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                    bool last, int kv, float* rec, int rs, float* grec = nullptr,
-                                                    long long gs = 0) {
+                                                    bool last, int kv, float* rec, int rs, float* grec, int gs) {
     if (kv == RW * (2 * R + 1))
         chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs, grec, gs);
     else
@@ -851,7 +851,7 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     pdl_wait();  // the pass input is the previous pass's output
     if (!late) pdl_trigger();
     if (L < NL && wid < nw) {
-        const int img = L / g.nb, b = L - img * g.nb;
+        const int img = g.batch == 1 ? 0 : L / g.nb, b = L - img * g.nb;  // no integer division for one image
         const int lo = band_lo(g, b);
         const int y0 = j * RW;
         const int nrows = min(RW, g.Hl - y0);
@@ -860,11 +860,11 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
                                  nullptr, L);
         // every chunk record also goes to HBM for KC / KB (nothing downstream redoes the spike-forward)
         chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0 || g.has_prev, j == g.P - 1 && !g.has_next, nrows * M, rec, rs,
-                                          crec + (long long)j * RL::REC * NL + L, (long long)NL);
+                                          crec + (long long)j * RL::REC * NL + L, NL);
     }
     __syncthreads();
     if (late) pdl_trigger();
-    const int PS = (g.P + NW - 1) / NW;
+    const int PS = jfast ? gridDim.x : gridDim.y;  // = ceil(P / NW), the grid's tile dimension
     if (wid == 0 && L < NL) {
         const long long NLl = NL;
         reduce_super<R, C>(sm + lane, rs, 32, nw, J == 0 && !g.has_prev, J == PS - 1 && !g.has_next,
@@ -1130,7 +1130,7 @@ __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, in
 #define SGWLS_KC_MINB 1
 #endif
 template <int R, int C>
-__global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g, int NWA, const float* __restrict__ crec,
+__global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g, int NWA, int PSA, const float* __restrict__ crec,
                                                 const float* __restrict__ zs, float* __restrict__ sep) {
     using RL = Rec<R, C>;
     extern __shared__ float sm[];
@@ -1140,7 +1140,6 @@ __global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g,
     const long long NLl = NL;
     const int L = blockIdx.x * 32 + lane;
     const int J = blockIdx.y * NTY + ty;
-    const int PSA = (g.P + NWA - 1) / NWA;
     pdl_wait();  // K2's super-separators (and, through K2, KA's records)
     pdl_trigger();
     if (L >= NL || J >= PSA) return;
@@ -1463,7 +1462,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const bool lastc = (j == g.P - 1) && !g.has_next;
     const bool has_left = j > 0 || g.has_prev;
     if constexpr (INNER) {
-        const int PS = (g.P + NW - 1) / NW;
+        const int PS = to.jfast ? gridDim.x : gridDim.y;  // = ceil(P / NW)
         __syncthreads();
         // ---- 2. lane-per-band solve of the tile's inner separators with the
         //         two known super-separators as boundary values
@@ -1780,7 +1779,7 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             e = cudaFuncSetAttribute(kc_inner<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
             if (e != cudaSuccess) return e;
             e = launch_pdl(kc_inner<R, C>, dim3((NL + 31) / 32, (PSA + nty - 1) / nty), dim3(32, nty), smc, st, g, NWA,
-                           (const float*)pl.crec, (const float*)pl.z, pl.sep);
+                           PSA, (const float*)pl.crec, (const float*)pl.z, pl.sep);
             if (e != cudaSuccess) return e;
         }
     }
