@@ -750,7 +750,7 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     const long long NLl = NL;
     const int PSn = g.P;  // super records
     const int NGa = min(NG, PSn);
-    const int J0 = (int)((long long)w * PSn / NGa), J1 = (int)((long long)(w + 1) * PSn / NGa);
+    const int J0 = w * PSn / NGa, J1 = (w + 1) * PSn / NGa;  // 32-bit: PSn * NG < 2^31
     const int gsz = J1 - J0;
     const int rsG = NG * 32 + 1;
     float* grec = sm;
@@ -1208,7 +1208,7 @@ __global__ void __launch_bounds__(512) k2_slab_reduce(const PassGeom g, int PS, 
     const int L = blockIdx.x * 32 + lane;
     const bool ok = L < NL;
     const int NGa = min(NG, PS);
-    const int J0 = (int)((long long)w * PS / NGa), J1 = (int)((long long)(w + 1) * PS / NGa);
+    const int J0 = w * PS / NGa, J1 = (w + 1) * PS / NGa;
     const int rsG = NG * 32 + 1;
     pdl_wait();  // KA's super-records
     pdl_trigger();
@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(512) k2_slab_solve(const PassGeom g, int PS, i
     const int L = blockIdx.x * 32 + lane;
     const bool ok = L < NL;
     const int NGa = min(NG, PS);
-    const int J0 = (int)((long long)w * PS / NGa), J1 = (int)((long long)(w + 1) * PS / NGa);
+    const int J0 = w * PS / NGa, J1 = (w + 1) * PS / NGa;
     float* zgrp = sm;                         // (NG + 1) x R*C x 32: [0] = zL, [k+1] = group k's separator
     float* bs2 = zgrp + (NG + 1) * R * C * 32;  // NG x R x RS x 32
     pdl_wait();
@@ -1391,7 +1391,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const bool last_cta = B0 + 32 >= g.nb;
 #ifndef SGWLS_NO_SHFL_AVG
     const bool shfl_avg = to.nph > 1 && g.tau <= 3 && bl < g.nreg &&
-                          (!last_cta || (bl - B0) + (M - 1) / g.tau <= 31);
+                          (!last_cta || (bl - B0) + div_tau(g, M - 1) <= 31);
 #else
     const bool shfl_avg = false;
 #endif
