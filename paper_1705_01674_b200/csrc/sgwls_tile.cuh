@@ -183,7 +183,7 @@ struct ChunkIn {
     float w[K][R];  // w[k][t-1] = lambda * weight of edge (k - t, k)
 };
 
-template <int R, int C, int CG, int RW, int WK>
+template <int R, int C, int CG, int RW, int WK, bool FULLC>
 __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
                                              const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
                                              int lo, int y0, int nrows, unsigned long long* err, int line) {
@@ -204,29 +204,43 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
             for (int c = 0; c < CG; ++c) gprev[i][c] = 0.f;
         }
     }
+    // Each row's M samples are loaded in memory order from one base address
+    // (compile-time offsets, no per-sample address arithmetic) and the
+    // serpentine reversal of odd rows (proj/src/snake.cpp:21-49) is applied to
+    // the values.  With an even RW the row parity is compile-time (chunks start
+    // on even rows).  FULLC: every row of the chunk exists (no predicates).
+    const float* rowF = F + ((long long)y0 * g.Wl + lo) * C;
+    const float* rowG = G + ((long long)y0 * g.Wl + lo) * CG;
+    const long long stF = (long long)g.Wl * C, stG = (long long)g.Wl * CG;
 #pragma unroll
     for (int rr = 0; rr < RW; ++rr) {
-        const int y = y0 + rr;
-        const bool valid = rr < nrows;
-        const bool odd = y & 1;
-        const float* rowF = F + ((long long)y * g.Wl + lo) * C;
-        const float* rowG = G + ((long long)y * g.Wl + lo) * CG;
+        const bool valid = FULLC || rr < nrows;
+        const bool odd = (RW % 2 == 0) ? ((rr & 1) != 0) : (((y0 + rr) & 1) != 0);
+        float vf[M][C], vg[M][CG];
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            if (valid) {
+#pragma unroll
+                for (int c = 0; c < C; ++c) vf[jj][c] = __ldg(rowF + jj * C + c);
+#pragma unroll
+                for (int c = 0; c < CG; ++c) vg[jj][c] = __ldg(rowG + jj * CG + c);
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) vf[jj][c] = 0.f;
+#pragma unroll
+                for (int c = 0; c < CG; ++c) vg[jj][c] = 0.f;
+            }
+        }
 #pragma unroll
         for (int jj = 0; jj < M; ++jj) {
             const int k = rr * M + jj;
-            const int co = odd ? (M - 1 - jj) : jj;
-            if (valid) {
 #pragma unroll
-                for (int c = 0; c < C; ++c) in.f[k][c] = __ldg(rowF + co * C + c);
+            for (int c = 0; c < C; ++c) in.f[k][c] = odd ? vf[M - 1 - jj][c] : vf[jj][c];
 #pragma unroll
-                for (int c = 0; c < CG; ++c) gp[k][c] = __ldg(rowG + co * CG + c);
-            } else {
-#pragma unroll
-                for (int c = 0; c < C; ++c) in.f[k][c] = 0.f;
-#pragma unroll
-                for (int c = 0; c < CG; ++c) gp[k][c] = 0.f;
-            }
+            for (int c = 0; c < CG; ++c) gp[k][c] = odd ? vg[M - 1 - jj][c] : vg[jj][c];
         }
+        rowF += stF;
+        rowG += stG;
     }
     // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time.
     // A NaN weight (NaN guidance) is the reference's "non-positive pivot" failure:
@@ -277,10 +291,21 @@ template <int R, int C, int CG, int RW>
 __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
                                            const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
                                            int lo, int y0, int nrows, unsigned long long* err, int line) {
+#ifndef SGWLS_NO_FULL_LOAD
+    if (W.kind == 1) {
+        if (nrows == RW)
+            load_chunk_k<R, C, CG, RW, 1, true>(in, F, G, g, W, lo, y0, nrows, err, line);
+        else
+            load_chunk_k<R, C, CG, RW, 1, false>(in, F, G, g, W, lo, y0, nrows, err, line);
+    } else {
+        load_chunk_k<R, C, CG, RW, 0, false>(in, F, G, g, W, lo, y0, nrows, err, line);
+    }
+#else
     if (W.kind == 1)
-        load_chunk_k<R, C, CG, RW, 1>(in, F, G, g, W, lo, y0, nrows, err, line);
+        load_chunk_k<R, C, CG, RW, 1, false>(in, F, G, g, W, lo, y0, nrows, err, line);
     else
-        load_chunk_k<R, C, CG, RW, 0>(in, F, G, g, W, lo, y0, nrows, err, line);
+        load_chunk_k<R, C, CG, RW, 0, false>(in, F, G, g, W, lo, y0, nrows, err, line);
+#endif
 }
 
 // ------------------------------------------------- elimination window (scalar)
