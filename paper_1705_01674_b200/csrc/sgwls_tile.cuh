@@ -1606,20 +1606,26 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     for (int jj = 0; jj < M; ++jj) csc[jj] = (active && !shfl_avg) ? fabsf(inv_col[lo - xa + jj]) : 0.f;
     for (int ph = 0; ph < (shfl_avg ? 0 : to.nph); ++ph) {
         if (active && (lane % to.nph) == ph) {
+            const bool first = to.nph == 1 || (store_first && ph == 0);  // first writer of every cell it touches
+            // column m of the band at tile column (lo - xa) + m: per-row stores at
+            // compile-time offsets from M column bases; the serpentine reversal of
+            // a row is applied to the values, not to the addresses
+            float* tcol[M];
 #pragma unroll
-            for (int p = 0; p < K; ++p) {
-                if (p < kv) {
-                    const int rr = p / M, jj = p % M;
-                    const int oe = jj * sx + rr * sy, oo = (M - 1 - jj) * sx + rr * sy;
+            for (int m = 0; m < M; ++m) tcol[m] = tbase + m * sx;
+#pragma unroll
+            for (int rr = 0; rr < RW; ++rr) {
+                if (rr * M < kv) {
                     const bool rev = (par0 ^ (rr & 1)) != 0;
-                    float* tp = tbase + (rev ? oo : oe);
-                    const float sc = rev ? csc[M - 1 - jj] : csc[jj];
-                    if (to.nph == 1 || (store_first && ph == 0)) {  // first writer of every cell it touches
+                    const int ro = rr * sy;
 #pragma unroll
-                        for (int c = 0; c < C; ++c) tp[c] = ys[p][c] * sc;
-                    } else {
+                    for (int m = 0; m < M; ++m) {
+                        float* tp = tcol[m] + ro;
 #pragma unroll
-                        for (int c = 0; c < C; ++c) tp[c] = fmaf(ys[p][c], sc, tp[c]);
+                        for (int c = 0; c < C; ++c) {
+                            const float v = rev ? ys[rr * M + (M - 1 - m)][c] : ys[rr * M + m][c];
+                            tp[c] = first ? v * csc[m] : fmaf(v, csc[m], tp[c]);
+                        }
                     }
                 }
             }
