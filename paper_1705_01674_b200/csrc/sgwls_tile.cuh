@@ -847,7 +847,12 @@ template <int R, int C, int CG>
 #define SGWLS_KB_MINB_KC (C == 1 ? 4 : 3)
 #endif
 // the INNER variant (r = 1) spills badly under a tighter budget: 2 CTAs (<= 128)
-#define SGWLS_KB_BOUNDS __launch_bounds__(256, (INNER ? 2 : SGWLS_KB_MINB_KC))
+#ifndef SGWLS_KB_MINB_INNER
+// the r = 1 INNER KB: <= 85 registers for one channel (c1 +2.3 %), <= 128 with
+// several (3 CTAs spill: c2 -16 %)
+#define SGWLS_KB_MINB_INNER (C == 1 ? 3 : 2)
+#endif
+#define SGWLS_KB_BOUNDS __launch_bounds__(256, (INNER ? SGWLS_KB_MINB_INNER : SGWLS_KB_MINB_KC))
 __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
                                                float* __restrict__ rsc, float* __restrict__ zs,
