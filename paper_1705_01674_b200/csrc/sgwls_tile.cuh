@@ -611,11 +611,27 @@ __device__ __forceinline__ void enter_block(BWin<R, C, SPIKE>& w, const float* t
 }
 
 // Reduce the NW chunk records of one band (lane) to its super-chunk record.
+// L1 prefetch of record s of a GLOBAL record run (every field: one 128-byte
+// line per warp when the lanes are consecutive lines).  The serial loops below
+// otherwise wait a full L2/HBM round trip per record.
+#ifndef SGWLS_REC_PF
+#define SGWLS_REC_PF 4  // records ahead (0 = off); used for r >= 2 (c3 +1.3 %, c4 +1 %, c5 +2 %;
+                        // the r = 1 K2 of c2 loses 3.6 % with it)
+#endif
 template <int R, int C>
+__device__ __forceinline__ void prefetch_record(const float* recs, long long rs, long long cs, int s) {
+#pragma unroll
+    for (int f = 0; f < Rec<R, C>::REC; ++f)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(recs + (long long)s * cs + (long long)f * rs));
+}
+
+template <int R, int C, bool GPF = false>
 __device__ __forceinline__ void reduce_super(const float* recs, long long rs, long long cs, int nw, bool first_super,
                                              bool last_super, float* out, long long os) {
-    // recs: chunk s's field f at recs[s * cs + f * rs]
+    // recs: chunk s's field f at recs[s * cs + f * rs]; GPF: recs is global, prefetch ahead
     using RL = Rec<R, C>;
+    if (GPF && SGWLS_REC_PF > 0)
+        for (int s = 0; s < min(nw, SGWLS_REC_PF); ++s) prefetch_record<R, C>(recs, rs, cs, s);
     BWin<R, C, true> w;
     w.clear_all();
     if (!first_super) {  // head of the tile's first chunk: update of the left super-separator
@@ -630,6 +646,7 @@ __device__ __forceinline__ void reduce_super(const float* recs, long long rs, lo
     }
     const int nblk = last_super ? nw - 1 : nw;  // separators of this tile's chunks
     for (int s = 0; s < nblk; ++s) {
+        if (GPF && SGWLS_REC_PF > 0 && s + SGWLS_REC_PF < nw) prefetch_record<R, C>(recs, rs, cs, s + SGWLS_REC_PF);
         const float* t = recs + (long long)s * cs;
         const float* h = recs + (long long)(s + 1) * cs;
         const bool inner = (s < nw - 1);  // sigma_s is internal (its next chunk is in the tile)
@@ -676,16 +693,19 @@ __device__ __forceinline__ void reduce_super(const float* recs, long long rs, lo
 // (has_l: zL, has_r: zR).  Record s's field f is at recs[s*cs + f*rs]; the
 // solution of inner separator s, component (q, c) goes to
 // zout[((s*R + q)*C + c) * zst]; back-substitution rows use bs (stride bss).
-template <int R, int C>
+template <int R, int C, bool GPF = false>
 __device__ __forceinline__ void solve_inner(const float* recs, long long rs, long long cs, int nw, bool has_l,
                                             const float (&zL)[R][C], bool has_r, const float (&zR)[R][C], float* zout,
                                             long long zst, float* bs, long long bss) {
     using RL = Rec<R, C>;
     const int nint = nw - 1;
     auto T = [&](int s) { return recs + (long long)s * cs; };
+    if (GPF && SGWLS_REC_PF > 0)
+        for (int s = 0; s < min(nw, SGWLS_REC_PF + 1); ++s) prefetch_record<R, C>(recs, rs, cs, s);
     BWin<R, C, false> w;
     w.clear_all();
     for (int s = 0; s < nint; ++s) {
+        if (GPF && SGWLS_REC_PF > 0 && s + 1 + SGWLS_REC_PF < nw) prefetch_record<R, C>(recs, rs, cs, s + 1 + SGWLS_REC_PF);
         enter_block<R, C, false>(w, T(s), T(s + 1), (int)rs, true, s > 0, s > 0);
         if (s == 0 && has_l) {  // known left separator: its coupling moves to the RHS
 #pragma unroll
@@ -783,7 +803,7 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     float* bsg = zg + NG * R * C * 32;
     const float* my = rec + (long long)J0 * RL::REC * NLl + L;
     if (w < NGa && ok)
-        reduce_super<R, C>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
+        reduce_super<R, C, (R >= 2)>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
     __syncthreads();
     float z0[R][C];
 #pragma unroll
@@ -809,7 +829,7 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-        solve_inner<R, C>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
+        solve_inner<R, C, (R >= 2)>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
                           z + (long long)J0 * R * C * NLl + L, NLl, rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
     }
 }
@@ -1196,7 +1216,7 @@ __global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g,
 #pragma unroll
             for (int c = 0; c < C; ++c) out[((long long)((nw - 1) * R + q) * C + c) * NLl] = zR[q][c];
     }
-    solve_inner<R, C>(crec + (long long)J * NWA * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, nw, has_l, zL,
+    solve_inner<R, C, (R >= 2)>(crec + (long long)J * NWA * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, nw, has_l, zL,
                       has_r, zR, out, NLl, sm + tid, NT);
 }
 
@@ -1244,7 +1264,7 @@ __global__ void __launch_bounds__(512) k2_slab_reduce(const PassGeom g, int PS, 
     pdl_trigger();
     if (w < NGa && ok) {
         float* gout = sm + w * 32 + lane;
-        reduce_super<R, C>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0,
+        reduce_super<R, C, (R >= 2)>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0,
                            w == 0 && !g.has_prev, w == NGa - 1 && !g.has_next, gout, rsG);
 #pragma unroll 1
         for (int f = 0; f < RL::REC; ++f) grec[((long long)w * RL::REC + f) * NLl + L] = gout[f * rsG];
@@ -1319,7 +1339,7 @@ __global__ void __launch_bounds__(512) k2_slab_solve(const PassGeom g, int PS, i
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-        solve_inner<R, C>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0, has_l, zL,
+        solve_inner<R, C, (R >= 2)>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0, has_l, zL,
                           has_r, zR, z + (long long)J0 * R * C * NLl + L, NLl,
                           rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
     }
