@@ -615,8 +615,8 @@ __device__ __forceinline__ void enter_block(BWin<R, C, SPIKE>& w, const float* t
 // line per warp when the lanes are consecutive lines).  The serial loops below
 // otherwise wait a full L2/HBM round trip per record.
 #ifndef SGWLS_REC_PF
-#define SGWLS_REC_PF 4  // records ahead (0 = off); used for r >= 2 (c3 +1.3 %, c4 +1 %, c5 +2 %;
-                        // the r = 1 K2 of c2 loses 3.6 % with it)
+#define SGWLS_REC_PF 2  // records ahead (0 = off); used for r >= 2 (vs none: c3 +4 %, c4 +1.4 %, c5 +2.3 %;
+                        // 2 beats 4 and 8; the r = 1 K2 of c2 loses 3.6 % with it)
 #endif
 template <int R, int C>
 __device__ __forceinline__ void prefetch_record(const float* recs, long long rs, long long cs, int s) {
