@@ -618,6 +618,9 @@ __device__ __forceinline__ void enter_block(BWin<R, C, SPIKE>& w, const float* t
 #define SGWLS_REC_PF 2  // records ahead (0 = off); used for r >= 2 (vs none: c3 +4 %, c4 +1.4 %, c5 +2.3 %;
                         // 2 beats 4 and 8; the r = 1 K2 of c2 loses 3.6 % with it)
 #endif
+#ifndef SGWLS_REC_PF_MINR
+#define SGWLS_REC_PF_MINR 2  // smallest radius that prefetches
+#endif
 template <int R, int C>
 __device__ __forceinline__ void prefetch_record(const float* recs, long long rs, long long cs, int s) {
 #pragma unroll
@@ -803,7 +806,7 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     float* bsg = zg + NG * R * C * 32;
     const float* my = rec + (long long)J0 * RL::REC * NLl + L;
     if (w < NGa && ok)
-        reduce_super<R, C, (R >= 2)>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
+        reduce_super<R, C, (R >= SGWLS_REC_PF_MINR)>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
     __syncthreads();
     float z0[R][C];
 #pragma unroll
@@ -829,7 +832,7 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-        solve_inner<R, C, (R >= 2)>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
+        solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
                           z + (long long)J0 * R * C * NLl + L, NLl, rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
     }
 }
@@ -1216,7 +1219,7 @@ __global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g,
 #pragma unroll
             for (int c = 0; c < C; ++c) out[((long long)((nw - 1) * R + q) * C + c) * NLl] = zR[q][c];
     }
-    solve_inner<R, C, (R >= 2)>(crec + (long long)J * NWA * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, nw, has_l, zL,
+    solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(crec + (long long)J * NWA * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, nw, has_l, zL,
                       has_r, zR, out, NLl, sm + tid, NT);
 }
 
@@ -1264,7 +1267,7 @@ __global__ void __launch_bounds__(512) k2_slab_reduce(const PassGeom g, int PS, 
     pdl_trigger();
     if (w < NGa && ok) {
         float* gout = sm + w * 32 + lane;
-        reduce_super<R, C, (R >= 2)>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0,
+        reduce_super<R, C, (R >= SGWLS_REC_PF_MINR)>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0,
                            w == 0 && !g.has_prev, w == NGa - 1 && !g.has_next, gout, rsG);
 #pragma unroll 1
         for (int f = 0; f < RL::REC; ++f) grec[((long long)w * RL::REC + f) * NLl + L] = gout[f * rsG];
@@ -1339,7 +1342,7 @@ __global__ void __launch_bounds__(512) k2_slab_solve(const PassGeom g, int PS, i
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-        solve_inner<R, C, (R >= 2)>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0, has_l, zL,
+        solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(srec + (long long)J0 * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, J1 - J0, has_l, zL,
                           has_r, zR, z + (long long)J0 * R * C * NLl + L, NLl,
                           rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
     }
