@@ -162,10 +162,15 @@ int sgwls_b200_slab_sizes(int width, int rows, int channels, int guidance_channe
 int sgwls_b200_slab_pass_a(const float* d_src, const float* d_guidance, int width, int rows, int channels,
                            int guidance_channels, int row0, int nslabs, int islab, const sgwls_b200_config* cfg,
                            float* d_work, float* d_record, void* stream, char* err, size_t errlen);
+/* d_pivot_err (device, may be NULL): a 64-bit word the caller sets to ~0 before the
+ * filter's FIRST pass; that pass's phase B lowers it (atomicMin) to (line << 32 | k)
+ * for the first position k of the reference's "non-positive pivot at row k"
+ * failure (proj/src/banded.cpp:66-68), k counted from the image's first row.
+ * The caller min-reduces the words of all slabs. */
 int sgwls_b200_slab_pass_b(const float* d_src, const float* d_guidance, int width, int rows, int channels,
                            int guidance_channels, int row0, int nslabs, int islab, const sgwls_b200_config* cfg,
-                           float* d_work, const float* d_records, float* d_out, void* stream, char* err,
-                           size_t errlen);
+                           float* d_work, const float* d_records, float* d_out, unsigned long long* d_pivot_err,
+                           void* stream, char* err, size_t errlen);
 
 /* ---- application pipelines (proj/include/sgwls/apps.hpp, proj/src/apps.cpp) ----
  * The reference's four callers of the filter, with every stage on the device:
@@ -205,6 +210,12 @@ int sgwls_b200_colorize(const float* gray, int gray_channels, const float* scrib
                         char* err, size_t errlen);
 
 const char* sgwls_b200_version(void);
+
+/* CUDA-graph cache of SGWLS_B200_GRAPH calls: an LRU of at most 64 entries per
+ * process.  _clear waits for and releases every cached graph (returns how many
+ * there were); _count reports the cache size. */
+int sgwls_b200_graph_clear(void);
+int sgwls_b200_graph_count(void);
 
 #ifdef __cplusplus
 }

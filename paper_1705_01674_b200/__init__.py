@@ -4,10 +4,12 @@ kernels behind a C ABI (include/sgwls_b200.h).  See DESIGN.md."""
 from .config import (Axis, CudaError, Error, SmoothConfig, SparseField, WeightKind, WeightParams,  # noqa: F401
                      orthogonal)
 from .api import (interpolate_sparse, interpolate_sparse_batch, interpolate_sparse_device,  # noqa: F401
-                  kernel_launches, pass_device, smooth, smooth_batch, smooth_device, validate, version)
+                  graph_clear, graph_count, kernel_launches, pass_device, smooth, smooth_batch, smooth_device,
+                  validate, version)
 from . import apps  # noqa: F401  (application pipelines, proj/src/apps.cpp)
 
 __all__ = ["Axis", "CudaError", "Error", "SmoothConfig", "SparseField", "WeightKind", "WeightParams",
            "orthogonal", "smooth", "smooth_batch", "smooth_device", "interpolate_sparse",
            "interpolate_sparse_batch", "interpolate_sparse_device", "validate", "kernel_launches", "version",
+           "graph_clear", "graph_count",
            "pass_device", "apps"]

@@ -93,6 +93,8 @@ SIGNATURES = {
     "sgwls_b200_profile_read": (C.c_int, [C.c_char_p, C.c_size_t]),
     "sgwls_b200_profile_collect": (None, []),
     "sgwls_b200_version": (C.c_char_p, []),
+    "sgwls_b200_graph_clear": (C.c_int, []),
+    "sgwls_b200_graph_count": (C.c_int, []),
     "sgwls_b200_transpose_device": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, _P, C.c_char_p,
                                               C.c_size_t]),
     # row-slab mode (slabs.py)
@@ -101,7 +103,7 @@ SIGNATURES = {
     "sgwls_b200_slab_pass_a": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(NativeConfig), _P, _P, _P, C.c_char_p, C.c_size_t]),
     "sgwls_b200_slab_pass_b": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                                         C.POINTER(NativeConfig), _P, _P, _P, _P, C.c_char_p, C.c_size_t]),
+                                         C.POINTER(NativeConfig), _P, _P, _P, _P, _P, C.c_char_p, C.c_size_t]),
     # application pipelines (proj/src/apps.cpp)
     "sgwls_b200_enhance_preset": (None, [C.POINTER(NativeConfig)]),
     "sgwls_b200_tonemap_layer_preset": (None, [C.c_double, C.POINTER(NativeConfig)]),

@@ -87,7 +87,21 @@ def interpolate_sparse(field: SparseField, guidance, cfg: SmoothConfig | None = 
     m = np.ascontiguousarray(m, dtype=np.float32)
     if m.shape != v.shape[:2]:
         raise Error("interpolate_sparse: values/mask size mismatch")
+    # field checks before smooth()'s own (proj/src/smoother.cpp:129-147): the
+    # first offending pixel in scan order decides the text
+    bad01 = (m != 0) & (m != 1)
+    offv = (m == 0) & np.any(v != 0, axis=2)
+    both = bad01 | offv
+    if both.any():
+        k = int(np.argmax(both.ravel()))
+        raise Error("interpolate_sparse: mask must be 0/1" if bad01.ravel()[k]
+                    else "interpolate_sparse: values nonzero outside mask")
+    if not (m == 1).any():
+        raise Error("interpolate_sparse: empty mask")
+    validate(cfg)
     g = _as_hwc(guidance, "interpolate_sparse")
+    if v.size == 0:
+        raise Error("smooth: empty target")
     if g.shape[:2] != v.shape[:2]:
         raise Error("smooth: target and guidance dimensions differ")
     h, w, c = v.shape
@@ -123,10 +137,14 @@ def interpolate_sparse_batch(values, masks, guidances, cfg: SmoothConfig | None 
 
 # ------------------------------------------------------------ device forms
 
-def _stream_ptr(stream) -> int:
+def _stream_ptr(stream, device) -> int:
+    """Raw handle of ``stream`` (default: the current stream of ``device``); the
+    stream must belong to the tensors' device."""
     import torch
 
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    if s.device != device:
+        raise Error(f"sgwls_b200: stream is on {s.device}, tensors are on {device}")
     return int(s.cuda_stream)
 
 
@@ -134,7 +152,7 @@ def _dev_dims(t, name):
     """(B, H, W, C) of a contiguous fp32 CUDA tensor shaped (H,W), (H,W,C) or (B,H,W,C)."""
     import torch
 
-    if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+    if not isinstance(t, torch.Tensor) or not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
         raise Error(f"{name}: expected a contiguous float32 CUDA tensor")
     if t.dim() == 2:
         return 1, t.shape[0], t.shape[1], 1
@@ -145,10 +163,29 @@ def _dev_dims(t, name):
     raise Error(f"{name}: bad tensor rank")
 
 
+def _same_device(name, ref, *ts):
+    for t in ts:
+        if t is not None and t.device != ref.device:
+            raise Error(f"{name}: all tensors must be on {ref.device} (got {t.device})")
+
+
+def _check_out(t, shape, ref, name):
+    """A caller-supplied output must be a contiguous fp32 tensor of exactly
+    ``shape`` on the inputs' device (the kernels write through a raw pointer)."""
+    import torch
+
+    if not isinstance(t, torch.Tensor) or not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise Error(f"{name}: expected a contiguous float32 CUDA tensor")
+    if tuple(t.shape) != tuple(shape):
+        raise Error(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    _same_device(name, ref, t)
+
+
 def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, stream=None, sync: bool = False,
                   graph: bool = False):
     """smooth on torch CUDA tensors, (H,W[,C]) or batched (B,H,W,C); stream-ordered.
-    graph=True captures the call into a CUDA graph once per (buffers, shape, config) and replays it."""
+    graph=True captures the call into a CUDA graph once per (buffers, shape, config) and replays it.
+    The kernels run on the tensors' device (made current for the call)."""
     import torch
 
     cfg = cfg or SmoothConfig()
@@ -156,13 +193,18 @@ def smooth_device(target, guidance, cfg: SmoothConfig | None = None, out=None, s
     bg, hg, wg, gc = _dev_dims(guidance, "smooth")
     if (hg, wg) != (h, w) or bg != b:
         raise Error("smooth: target and guidance dimensions differ")
+    _same_device("smooth", target, guidance)
     if out is None:
         out = torch.empty_like(target)
+    else:
+        _check_out(out, target.shape, target, "smooth: out")
     err = N.errbuf()
     nc = N.to_native(cfg)
     flags = (N.SYNC if sync else 0) | (N.GRAPH if graph else 0)
-    rc = N.lib().sgwls_b200_smooth_device(target.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
-                                          out.data_ptr(), _stream_ptr(stream), flags, err, len(err))
+    with torch.cuda.device(target.device):
+        rc = N.lib().sgwls_b200_smooth_device(target.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
+                                              out.data_ptr(), _stream_ptr(stream, target.device), flags, err,
+                                              len(err))
     N.check(rc, err)
     return out
 
@@ -178,14 +220,18 @@ def pass_device(src, guidance, cfg: SmoothConfig | None = None, out=None, stream
     bg, hg, wg, gc = _dev_dims(guidance, "pass")
     if (hg, wg) != (h, w) or bg != b:
         raise Error("smooth: target and guidance dimensions differ")
+    _same_device("pass", src, guidance)
+    shape = (w, h) if src.dim() == 2 else ((w, h, c) if src.dim() == 3 else (b, w, h, c))
     if out is None:
-        shape = (w, h) if src.dim() == 2 else ((w, h, c) if src.dim() == 3 else (b, w, h, c))
         out = torch.empty(shape, dtype=torch.float32, device=src.device)
+    else:
+        _check_out(out, shape, src, "pass: out")
     err = N.errbuf()
     nc = N.to_native(cfg)
     flags = (N.SYNC if sync else 0) | (N.GRAPH if graph else 0)
-    rc = N.lib().sgwls_b200_pass_device(src.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
-                                        out.data_ptr(), _stream_ptr(stream), flags, err, len(err))
+    with torch.cuda.device(src.device):
+        rc = N.lib().sgwls_b200_pass_device(src.data_ptr(), guidance.data_ptr(), b, w, h, c, gc, C.byref(nc),
+                                            out.data_ptr(), _stream_ptr(stream, src.device), flags, err, len(err))
     N.check(rc, err)
     return out
 
@@ -193,25 +239,47 @@ def pass_device(src, guidance, cfg: SmoothConfig | None = None, out=None, stream
 def interpolate_sparse_device(values, masks, guidances, cfg: SmoothConfig | None = None, out=None,
                               undefined=None, stream=None, sync: bool = False, validate: bool = False,
                               graph: bool = False):
-    """Batched interpolate_sparse on torch CUDA tensors (B,H,W) or (B,H,W,C); stream-ordered."""
+    """Batched interpolate_sparse on torch CUDA tensors: values (B,H,W) or (B,H,W,C), masks (B,H,W),
+    guidances (B,H,W) or (B,H,W,Cg); out like values, undefined (B,H,W).  Stream-ordered.
+    validate=True runs the reference's field checks (mask 0/1, values zero off the mask, non-empty
+    mask) on the device for every pair, with one host synchronisation."""
     import torch
 
     cfg = cfg or SmoothConfig()
+    for t, nm in ((values, "values"), (masks, "masks"), (guidances, "guidances")):
+        _dev_dims(t, f"interpolate_sparse: {nm}")
     if values.dim() == 3:
         b, h, w = values.shape
         c = 1
-    else:
+    elif values.dim() == 4:
         b, h, w, c = values.shape
-    gc = 1 if guidances.dim() == 3 else guidances.shape[3]
+    else:
+        raise Error("interpolate_sparse: values must be (B,H,W) or (B,H,W,C)")
+    if masks.dim() != 3 or tuple(masks.shape) != (b, h, w):
+        raise Error("interpolate_sparse: values/mask size mismatch")
+    if guidances.dim() == 3:
+        gshape, gc = tuple(guidances.shape), 1
+    elif guidances.dim() == 4:
+        gshape, gc = tuple(guidances.shape[:3]), guidances.shape[3]
+    else:
+        raise Error("interpolate_sparse: guidances must be (B,H,W) or (B,H,W,Cg)")
+    if gshape != (b, h, w):
+        raise Error("smooth: target and guidance dimensions differ")
+    _same_device("interpolate_sparse", values, masks, guidances)
     if out is None:
         out = torch.empty_like(values)
+    else:
+        _check_out(out, values.shape, values, "interpolate_sparse: out")
+    if undefined is not None:
+        _check_out(undefined, (b, h, w), values, "interpolate_sparse: undefined")
     und_ptr = undefined.data_ptr() if undefined is not None else None
     err = N.errbuf()
     nc = N.to_native(cfg)
     flags = (N.SYNC if sync else 0) | (N.VALIDATE if validate else 0) | (N.GRAPH if graph else 0)
-    rc = N.lib().sgwls_b200_interpolate_sparse_device(values.data_ptr(), masks.data_ptr(), guidances.data_ptr(), b,
-                                                      w, h, c, gc, C.byref(nc), out.data_ptr(), und_ptr,
-                                                      _stream_ptr(stream), flags, err, len(err))
+    with torch.cuda.device(values.device):
+        rc = N.lib().sgwls_b200_interpolate_sparse_device(values.data_ptr(), masks.data_ptr(), guidances.data_ptr(),
+                                                          b, w, h, c, gc, C.byref(nc), out.data_ptr(), und_ptr,
+                                                          _stream_ptr(stream, values.device), flags, err, len(err))
     N.check(rc, err)
     return out
 
@@ -227,6 +295,15 @@ def kernel_launches(width, height, channels, guidance_channels, batch, sparse, c
     nc = N.to_native(cfg)
     return int(N.lib().sgwls_b200_kernel_launches(width, height, channels, guidance_channels, batch,
                                                   1 if sparse else 0, C.byref(nc)))
+
+
+def graph_clear() -> int:
+    """Release every cached CUDA graph of graph=True calls (waits for their last replay)."""
+    return int(N.lib().sgwls_b200_graph_clear())
+
+
+def graph_count() -> int:
+    return int(N.lib().sgwls_b200_graph_count())
 
 
 def version() -> str:

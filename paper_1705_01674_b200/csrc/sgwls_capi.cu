@@ -126,7 +126,10 @@ void build_weights(const sgwls_b200_config* c, WeightDev& w) {
     w.kind = c->weight_kind;
     w.lam = (float)c->lambda;
     const double log2e = 1.4426950408889634;
-    w.exp_k = (float)(-(c->guidance_scale * c->guidance_scale) * log2e / (2.0 * c->sigma_r * c->sigma_r));
+    // clamped to the finite range: an exponent that overflows float must not
+    // turn range = 0 (a flat guidance region) into 0 * -inf = NaN
+    const double ek = -(c->guidance_scale * c->guidance_scale) * log2e / (2.0 * c->sigma_r * c->sigma_r);
+    w.exp_k = ek < -3.4e38 ? -3.4e38f : (float)ek;
     w.frac_half = (float)(c->alpha_r * 0.5);
     w.frac_lg2s = (float)std::log2(c->guidance_scale * c->guidance_scale);
     w.eps = (float)c->epsilon;
@@ -149,8 +152,8 @@ struct AxisPlan {
     PassGeom g;
     int kmax;
     int bx;
-    int fast, step, ncta, nw, nph, nwa = 8, kc = 0;
-    size_t rec_n, rs_n, z_n, u_n, crec_n = 0, sep_n = 0;
+    int fast, step, ncta, nw, nph, nwa = 8;
+    size_t rec_n, rs_n, z_n, u_n, map_n = 0;
 };
 
 
@@ -212,15 +215,10 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
             const int n = v ? std::atoi(v) : 0;
             return n < 0 ? 0 : (n > 8 ? 8 : n);
         }();
-        static const int kc_env = [] {
-            const char* v = std::getenv("SGWLS_KC");  // tuning knob: 1/0 force the KC path on/off
-            return v ? std::atoi(v) : -1;
-        }();
-        // measured on B200: r = 1 -> one launch fewer (KB solves its tile's inner
-        // separators), 8-chunk tiles; r >= 2 -> KC, 4-chunk KB tiles and 8-chunk
-        // KA tiles (4 with several right-hand sides)
-        ap.kc = kc_env >= 0 ? kc_env : (r >= 2 ? 1 : 0);
-        ap.nwa = ap.kc ? (ka_warps_env ? ka_warps_env : (C >= 2 ? kTileWarps / 2 : kTileWarps)) : ap.nw;
+        // KA tiles (separator maps) and KB tiles are independent; measured
+        // schedule of round 1 kept: r >= 2: 8-chunk KA tiles for one channel,
+        // 4 with several right-hand sides; r = 1: as the KB tiles
+        ap.nwa = ka_warps_env ? ka_warps_env : (r == 1 ? ap.nw : (C >= 2 ? kTileWarps / 2 : kTileWarps));
         const int PS = (P + ap.nwa - 1) / ap.nwa;
         // halo: widest span of bands covering one column (incl. the forced last centre)
         int hspan = 0;
@@ -247,10 +245,9 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         }
         ap.nph = nph;
         ap.rec_n = P > 1 ? (size_t)PS * rec_floats(r, C) * NL : 0;
-        ap.crec_n = P > 1 ? (size_t)P * rec_floats(r, C) * NL : 0;
+        ap.map_n = P > 1 ? (size_t)P * map_floats(r, C) * NL : 0;
         ap.rs_n = PS > 1 ? (size_t)(PS - 1) * r * rs_floats(r, C) * NL : 0;
         ap.z_n = PS > 1 ? (size_t)(PS - 1) * r * C * NL : 0;
-        ap.sep_n = (P > 1 && ap.kc) ? (size_t)(P - 1) * r * C * NL : 0;
         ap.u_n = 0;
         return ap;
     }
@@ -275,27 +272,11 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
     return ap;
 }
 
-// Ready-flag mode (sgwls_device.cuh kFlagMaxSuper): r = 1 schedule with a
-// short reduced system; the K2 solve runs in KA and KB waits per band group.
-bool flag_mode(const AxisPlan& ap) {
-    static const int env = [] {
-        // tuning knob: 1 = ready-flag mode (measured on B200: c1 -17%, c2 +2% with
-        // SGWLS_KA_JFAST=SGWLS_KB_JFAST=1), so off by default
-        const char* v = std::getenv("SGWLS_FLAGS");
-        return v ? std::atoi(v) : 0;
-    }();
-    if (!env || !ap.fast || ap.kc || ap.g.P <= 1) return false;
-    const int PS = (ap.g.P + ap.nwa - 1) / ap.nwa;
-    return PS > 1 && PS <= kFlagMaxSuper;
-}
-
 int kernels_per_pass(const AxisPlan& ap) {
-    if (ap.fast) {  // ka_tile (K2 fused or its own k2_tree), kb_tile
-        if (flag_mode(ap)) return 2;
+    if (ap.fast) {
         const int PS = (ap.g.P + ap.nwa - 1) / ap.nwa;
-        static const int fuse_k2 = std::getenv("SGWLS_FUSE_K2") ? std::atoi(std::getenv("SGWLS_FUSE_K2")) : 0;
-        // ka_tile [+ k2_tree unless fused] [+ kc_inner] when the lines have several chunks; kb_tile
-        return (ap.g.P > 1 ? (1 + (ap.kc ? 1 : 0) + ((PS > 1 && !(fuse_k2 && tile_fuse_k2(PS))) ? 1 : 0)) : 0) + 1;
+        // ka_tile [+ k2_tree] when the lines have several chunks; kb_tile
+        return (ap.g.P > 1 ? (1 + (PS > 1 ? 1 : 0)) : 0) + 1;
     }
     return (ap.g.P > 1 ? 2 : 0) + 2;
 }
@@ -350,31 +331,24 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
     AxisPlan ap0 = plan_axis(H, W, C, Cg, cfg->r, cfg->tau, batch);  // column passes
     AxisPlan ap1 = plan_axis(W, H, C, Cg, cfg->r, cfg->tau, batch);  // row passes (transposed layout)
     auto mx = [](size_t a, size_t b) { return a > b ? a : b; };
-    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0, crec_n = 0, sep_n = 0;
+    size_t rec_n = 0, rs_n = 0, z_n = 0, u_n = 0, map_n = 0;
     if (need0) {
         rec_n = mx(rec_n, ap0.rec_n);
-        crec_n = mx(crec_n, ap0.crec_n);
-        sep_n = mx(sep_n, ap0.sep_n);
+        map_n = mx(map_n, ap0.map_n);
         rs_n = mx(rs_n, ap0.rs_n);
         z_n = mx(z_n, ap0.z_n);
         u_n = mx(u_n, ap0.u_n);
     }
     if (need1) {
         rec_n = mx(rec_n, ap1.rec_n);
-        crec_n = mx(crec_n, ap1.crec_n);
-        sep_n = mx(sep_n, ap1.sep_n);
+        map_n = mx(map_n, ap1.map_n);
         rs_n = mx(rs_n, ap1.rs_n);
         z_n = mx(z_n, ap1.z_n);
         u_n = mx(u_n, ap1.u_n);
     }
     const size_t img_n = (size_t)batch * W * H * C;
-    const size_t ngroups = (size_t)(mx(ap0.g.nb, ap1.g.nb) * batch + 31) / 32;
-    DevBuf rec, rs, z, U, bufA, bufB, gt, cnt, crec;
-    crec.alloc(crec_n, st);
-    DevBuf sepb;
-    sepb.alloc(sep_n, st);
-    cnt.alloc(2 * ngroups, st);  // [fused-K2 tile counters | ready flags]
-    CK(cudaMemsetAsync(cnt.p, 0, 2 * ngroups * sizeof(float), st));
+    DevBuf rec, rs, z, U, bufA, bufB, gt, maps;
+    maps.alloc(map_n, st);
     rec.alloc(rec_n, st);
     rs.alloc(rs_n, st);
     z.alloc(z_n, st);
@@ -405,20 +379,9 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.ncta = ap.ncta;
         pl.nw = ap.nw;
         pl.nwa = ap.nwa;
-        pl.kc = ap.kc;
-        pl.sep = sepb.p;
+
         pl.nph = ap.nph;
-        static const int fuse_k2 = [] {
-            // tuning knob: 1 = the last KA tile of a band group solves short reduced
-            // systems in place (measured neutral to -2% on B200, so off by default)
-            const char* v = std::getenv("SGWLS_FUSE_K2");
-            return v ? std::atoi(v) : 0;
-        }();
-        const bool flagged = flag_mode(ap);
-        pl.counters = (fuse_k2 || flagged) ? reinterpret_cast<int*>(cnt.p) : nullptr;
-        pl.flags = flagged ? reinterpret_cast<int*>(cnt.p) + ngroups : nullptr;
-        pl.epoch = p + 1;
-        pl.crec = crec.p;
+        pl.maps = maps.p;
         pl.src = src;
         pl.guid = o == 0 ? d_g : gt.p;
         const bool lastp = (p == T - 1);
@@ -438,15 +401,6 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.err = (p == 0) ? d_err : nullptr;
         pl.w = &wd;
         CK(launch_pass(pl, st));
-        if (p == 0 && std::getenv("SGWLS_DEBUG_Z") && z.p && z_n) {  // debugging aid: dump pass-0 separators
-            std::vector<float> hz(z_n);
-            CK(cudaMemcpyAsync(hz.data(), z.p, z_n * sizeof(float), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (FILE* f = std::fopen(std::getenv("SGWLS_DEBUG_Z"), "wb")) {
-                std::fwrite(hz.data(), sizeof(float), z_n, f);
-                std::fclose(f);
-            }
-        }
         src = out;
     }
 }
@@ -526,15 +480,42 @@ void finish_sync(unsigned long long* d_err, cudaStream_t st) {
 // by (pointers, shape, configuration) and replayed on later calls with the
 // same key: one launch per call instead of ~4 per pass, no host gaps.  The
 // graph runs on a private stream joined to the caller's stream with events.
+// The cache is a small LRU (kGraphCacheMax entries): an evicted entry waits for
+// its last replay and releases its exec, stream, events and error word.
 struct GraphEntry {
     cudaGraphExec_t exec = nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     unsigned long long* d_err = nullptr;
     int armed = 0;
+    unsigned long long used = 0;  // LRU stamp
+    int dev = 0;
+    ~GraphEntry() {
+        int cur = 0;
+        cudaGetDevice(&cur);
+        if (cur != dev) cudaSetDevice(dev);
+        if (st) cudaStreamSynchronize(st);
+        if (exec) cudaGraphExecDestroy(exec);
+        if (ev_in) cudaEventDestroy(ev_in);
+        if (ev_out) cudaEventDestroy(ev_out);
+        if (d_err) cudaFree(d_err);
+        if (st) cudaStreamDestroy(st);
+        if (cur != dev) cudaSetDevice(cur);
+    }
 };
+constexpr size_t kGraphCacheMax = 64;
 std::mutex g_graph_mu;
 std::map<std::string, std::unique_ptr<GraphEntry>> g_graphs;
+unsigned long long g_graph_clock = 0;
+
+void graph_evict_lru_locked() {
+    while (g_graphs.size() >= kGraphCacheMax) {
+        auto victim = g_graphs.begin();
+        for (auto it = g_graphs.begin(); it != g_graphs.end(); ++it)
+            if (it->second->used < victim->second->used) victim = it;
+        g_graphs.erase(victim);
+    }
+}
 
 std::string graph_key(const void* const* ptrs, int nptr, const int* dims, int ndims, const sgwls_b200_config* cfg,
                       int kind) {
@@ -554,9 +535,11 @@ std::string graph_key(const void* const* ptrs, int nptr, const int* dims, int nd
 template <class F>
 void run_graphed(const std::string& key, cudaStream_t user, bool sync, F&& body) {
     std::lock_guard<std::mutex> lk(g_graph_mu);
+    if (g_graphs.find(key) == g_graphs.end()) graph_evict_lru_locked();
     std::unique_ptr<GraphEntry>& slot = g_graphs[key];
     if (!slot) {
         auto ge = std::make_unique<GraphEntry>();
+        CK(cudaGetDevice(&ge->dev));
         CK(cudaStreamCreateWithFlags(&ge->st, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ge->ev_in, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ge->ev_out, cudaEventDisableTiming));
@@ -571,6 +554,7 @@ void run_graphed(const std::string& key, cudaStream_t user, bool sync, F&& body)
             prof_set_capture(nullptr);
             cudaStreamEndCapture(ge->st, &graph);
             if (graph) cudaGraphDestroy(graph);
+            g_graphs.erase(key);
             throw;
         }
         prof_set_capture(nullptr);
@@ -581,6 +565,7 @@ void run_graphed(const std::string& key, cudaStream_t user, bool sync, F&& body)
         slot = std::move(ge);
     }
     GraphEntry& ge = *slot;
+    ge.used = ++g_graph_clock;
     CK(cudaEventRecord(ge.ev_in, user));
     CK(cudaStreamWaitEvent(ge.st, ge.ev_in, 0));
     CK(cudaGraphLaunch(ge.exec, ge.st));
@@ -615,7 +600,7 @@ int guarded(char* err, size_t errlen, F&& f) {
 // (sgwls_tile.cuh "row-slab mode", sharded.py).
 struct SlabLayout {
     AxisPlan ap;
-    size_t crec = 0, srec = 0, rsc = 0, zext = 0, sepext = 0, zg = 0, bsg = 0, grec = 0, total = 0, record = 0;
+    size_t maps = 0, srec = 0, rsc = 0, zext = 0, zg = 0, bsg = 0, grec = 0, total = 0, record = 0;
 };
 
 SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_config* cfg, int nslabs) {
@@ -625,7 +610,7 @@ SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_conf
         throw Fail{SGWLS_B200_EUNSUPPORTED, "sgwls_b200: row-slab mode needs the tiled path (r <= 4, 1 or 3 guidance "
                                             "channels, width >= 2r+1)"};
     const size_t NL = L.ap.g.nb, r = cfg->r, REC = rec_floats(cfg->r, C), RS = rs_floats(cfg->r, C);
-    const size_t P = L.ap.g.P, NWA = L.ap.kc ? L.ap.nwa : L.ap.nw, PS = (P + NWA - 1) / NWA;
+    const size_t P = L.ap.g.P, NWA = L.ap.nwa, PS = (P + NWA - 1) / NWA;
     const size_t G = nslabs > 1 ? nslabs - 1 : 1;
     size_t off = 0;
     auto take = [&](size_t n) {
@@ -633,11 +618,10 @@ SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_conf
         off += (n + 31) & ~(size_t)31;
         return o;
     };
-    L.crec = take(P * REC * NL);
+    L.maps = take(P * map_floats(cfg->r, C) * NL);
     L.srec = take(PS * REC * NL);
     L.rsc = take((PS > 1 ? PS - 1 : 1) * r * RS * NL);
     L.zext = take((PS + 1) * r * C * NL);
-    L.sepext = take((P + 1) * r * C * NL);
     L.zg = take(G * r * C * NL);
     L.bsg = take(G * r * RS * NL);
     L.grec = take((size_t)kSlabWarps * REC * NL);
@@ -671,7 +655,6 @@ PassLaunch slab_launch(const SlabLayout& L, const float* src, const float* guid,
     pl.ncta = ap.ncta;
     pl.nw = ap.nw;
     pl.nwa = ap.nwa;
-    pl.kc = ap.kc;
     pl.nph = ap.nph;
     pl.kmax = ap.kmax;
     pl.src = src;
@@ -680,11 +663,10 @@ PassLaunch slab_launch(const SlabLayout& L, const float* src, const float* guid,
     pl.err = nullptr;
     pl.U = nullptr;
     const size_t NL = ap.g.nb, rC = (size_t)ap.g.r * C;
-    pl.crec = work + L.crec;
+    pl.maps = work + L.maps;
     pl.rec = work + L.srec;
     pl.rs = work + L.rsc;
     pl.z = work + L.zext + rC * NL;      // one slot in front: z[-1]
-    pl.sep = work + L.sepext + rC * NL;  // one slot in front: sep[-1]
     pl.zg = work + L.zg;
     pl.bsg = work + L.bsg;
     pl.grec = work + L.grec;
@@ -836,6 +818,10 @@ int sgwls_b200_interpolate_sparse_batch(const float* v, const float* m, const fl
                                         float* out, float* und, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         std::string msg;
+        // a field without pixels fails the reference's mask scan first
+        // (proj/src/smoother.cpp:131-144): "empty mask", before smooth()'s checks
+        if (batch >= 1 && channels >= 1 && (width <= 0 || height <= 0))
+            throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
         int rc = check_shape(batch, width, height, channels + 1, gch, msg);
         if (rc) throw Fail{rc, msg};
         require_device();
@@ -906,7 +892,19 @@ int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, i
     return ap.g.nb;
 }
 
-const char* sgwls_b200_version(void) { return "sgwls_b200 0.1.0 (sm_100a)"; }
+const char* sgwls_b200_version(void) { return "sgwls_b200 0.2.0 (sm_100a)"; }
+
+int sgwls_b200_graph_clear(void) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    const int n = (int)g_graphs.size();
+    g_graphs.clear();
+    return n;
+}
+
+int sgwls_b200_graph_count(void) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    return (int)g_graphs.size();
+}
 
 // ------------------------------------------------------------ row-slab mode
 
@@ -948,7 +946,8 @@ int sgwls_b200_slab_pass_a(const float* d_src, const float* d_guid, int width, i
 
 int sgwls_b200_slab_pass_b(const float* d_src, const float* d_guid, int width, int rows, int channels, int gch,
                            int row0, int nslabs, int islab, const sgwls_b200_config* cfg, float* d_work,
-                           const float* d_records, float* d_out, void* stream, char* err, size_t errlen) {
+                           const float* d_records, float* d_out, unsigned long long* d_pivot_err, void* stream,
+                           char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
         slab_check(width, rows, channels, gch, row0, nslabs, islab, cfg);
         require_device();
@@ -959,6 +958,7 @@ int sgwls_b200_slab_pass_b(const float* d_src, const float* d_guid, int width, i
         pl.slab_phase = 2;
         pl.slabrec = const_cast<float*>(d_records);
         pl.out = d_out;
+        pl.err = d_pivot_err;
         CK(launch_pass(pl, (cudaStream_t)stream));
     });
 }

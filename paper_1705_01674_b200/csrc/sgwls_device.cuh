@@ -98,15 +98,6 @@ __host__ __device__ constexpr int tile_rows_per_chunk(int R, int C) {
 }
 constexpr int kTileMaxR = 4;
 constexpr int kTileWarps = 8;
-// K2 runs inside the last KA tile of each band group when the reduced system
-// is this short (sequential depth ~2*PS/NW + NW); longer systems get their own
-// 16-warp tree launch.
-constexpr int kFuseK2MaxSuper = 32;
-__host__ __device__ constexpr bool tile_fuse_k2(int PS) { return PS > 1 && PS <= kFuseK2MaxSuper; }
-// Ready-flag mode (r = 1 schedule KA -> KB): the last KA tile of each band
-// group solves that group's reduced system (depth ~2*PS/NW + NW) and raises a
-// flag; KB tiles wait on their own groups' flags only.
-constexpr int kFlagMaxSuper = 64;
 // warps per band group of the row-slab reduce / solve kernels (sgwls_tile.cuh)
 constexpr int kSlabWarps = 16;
 
@@ -128,13 +119,21 @@ __device__ __forceinline__ float fast_rcp(float x) {
     return y;
 }
 
+// (range*gscale)^alpha_r = exp2(alpha_r/2 * (log2(range2) + log2(gscale^2)))
+// (proj/src/weights.cpp:67-71).  log2(0) = -inf is clamped to -FLT_MAX so that
+// range = 0 gives 0 for alpha_r > 0 and exactly 1 for alpha_r = 0, like
+// std::pow(0, alpha_r), instead of 0 * -inf = NaN.  A select, not fmaxf: a NaN
+// guidance must still give a NaN weight (the reference's pivot failure).
+__device__ __forceinline__ float frac_range_pow(const WeightDev& W, float range2) {
+    const float l = fast_lg2(range2) + W.frac_lg2s;
+    return fast_ex2(W.frac_half * (l < -3.402823466e38f ? -3.402823466e38f : l));
+}
+
 // Eq. 2 kernels on fp32 guidance (proj/src/weights.cpp:55-71).
 __device__ __forceinline__ float guidance_weight(const WeightDev& W, float range2, int d2) {
     const float s = W.spat[d2];
     if (W.kind == 1) return s * fast_ex2(range2 * W.exp_k);
-    // (range*gscale)^alpha_r = exp2(alpha_r/2 * (log2(range2) + log2(gscale^2))); log2(0) = -inf -> 0
-    const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
-    return s / (pr + W.eps);
+    return s / (frac_range_pow(W, range2) + W.eps);
 }
 
 // Same, with the kernel kind fixed at compile time (1 = Exp, 0 = Frac).
@@ -144,8 +143,7 @@ __device__ __forceinline__ float guidance_weight_k(const WeightDev& W, float ran
     if constexpr (WK == 1) {
         return s * fast_ex2(range2 * W.exp_k);
     } else {
-        const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
-        return s / (pr + W.eps);
+        return s / (frac_range_pow(W, range2) + W.eps);
     }
 }
 
@@ -157,8 +155,9 @@ __device__ __forceinline__ float guidance_lweight_k(const WeightDev& W, float ra
     if constexpr (WK == 1) {
         return fast_ex2(fmaf(range2, W.exp_k, W.lg2ls[d2]));
     } else {
-        const float pr = fast_ex2(W.frac_half * (fast_lg2(range2) + W.frac_lg2s));
-        return W.lspat[d2] / (pr + W.eps);
+        // approximate reciprocal (MUFU.RCP, <= 1 ulp) instead of the IEEE division
+        // and its slow path: pr + eps >= eps > 0, and rcp(inf) = 0
+        return W.lspat[d2] * fast_rcp(frac_range_pow(W, range2) + W.eps);
     }
 }
 

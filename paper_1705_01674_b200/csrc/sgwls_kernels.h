@@ -26,17 +26,9 @@ struct PassLaunch {
     float* U;           // band solutions
     unsigned long long* err;  // NaN-weight report (first pass only), or nullptr
     const WeightDev* w;
-    int* counters = nullptr;  // tiled path: per-band-group tile counters (zeroed; self-resetting)
-    float* crec = nullptr;    // tiled path: every chunk's record (KA -> KC), [chunk][field][line]
-    float* sep = nullptr;     // tiled path: every chunk separator (KC -> KB), [chunk][q][c][line]
-    int nwa = 8;              // tiled path: chunks per KA tile (super-chunk); == nw unless kc
-    int kc = 0;               // tiled path: separate KC launch for the chunk separators
-    // tiled path, ready-flag mode: KA's last tile per band group solves the
-    // group's reduced system and sets flags[group] = epoch; KB waits until its
-    // groups' flags reach epoch instead of waiting for the whole KA grid.
-    // The flags are zeroed once per call; pass p uses epoch p + 1.
-    int* flags = nullptr;
-    int epoch = 0;
+    float* maps = nullptr;    // tiled path: affine map of every inner chunk separator of a KA tile
+                              // (KA -> KB), [chunk][field][line], map_floats(r, C) fields
+    int nwa = 8;              // tiled path: chunks per KA tile (super-chunk)
     // tiled path, row-slab mode (geom.has_prev / has_next, sgwls_tile.cuh):
     // 1 = phase A (KA, then this slab's record -> slabrec), 2 = phase B (slabrec
     // = all nslab records; separators, KC, KB); z and sep then carry one slot in
@@ -52,6 +44,7 @@ struct PassLaunch {
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);
 size_t rec_floats(int r, int C);
 size_t rs_floats(int r, int C);
+size_t map_floats(int r, int C);
 cudaError_t launch_transpose(const float* in, float* out, int H, int W, int C, int batch, cudaStream_t st);
 cudaError_t launch_pack_sparse(const float* values, const float* mask, float* packed, long long npx, int C,
                                cudaStream_t st);

@@ -15,16 +15,17 @@
 //   KA ka_tile   spike-forward of every chunk -> chunk records in smem ->
 //                lane-per-band block elimination of the NW-1 inner separators
 //                carrying the spike toward the previous super-separator ->
-//                super-chunk record (same format as a chunk record).
-//   K2 k2_fast   sequential block-tridiagonal solve over super-separators
-//                (records prefetched), -> super-separator values.
-//   KB kb_tile   re-runs the chunk spike-forward (registers), solves the tile's
-//                inner separators with the two known super-separators as
-//                boundary values, then every chunk solves its interior with
-//                known separators (state in smem, back substitution in place),
-//                and the tile averages overlapping bands into a shared output
-//                tile in a fixed phase order (deterministic) and writes it in
-//                the next pass's transposed layout with coalesced stores.
+//                super-chunk record (same format as a chunk record), then the
+//                symbolic back substitution of the inner separators: each one
+//                as an affine map of the tile's two super-separators (HBM).
+//   K2 k2_tree   block-tridiagonal solve over the super-separators of a line,
+//                a tree over NG warps -> super-separator values.
+//   KB kb_tile   every chunk takes its two separators from KA's affine maps
+//                and the super-separators (a few FMAs), then solves its
+//                interior (forward elimination + back substitution in
+//                registers).  Overlapping bands are averaged in a fixed order
+//                (warp shuffles or a shared output tile) and the result leaves
+//                in the next pass's transposed layout.
 //
 // All eliminations: magnitudes + row-sum pivots (sgwls_device.cuh).
 #pragma once
@@ -37,7 +38,6 @@
 #include "sgwls_device.cuh"
 #include "sgwls_kernels.h"
 #include "sgwls_profile.h"
-#include "sgwls_fast.cuh"
 
 namespace sgwls_b200 {
 namespace tile {
@@ -64,19 +64,13 @@ __device__ __forceinline__ void bulk_commit_and_wait_read() {
 // order this thread's generic-proxy shared-memory writes before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// gpu-scope release store / acquire load of a ready flag
-__device__ __forceinline__ void st_release_gpu(int* p, int v) {
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+// 4-byte asynchronous global -> shared copy (LDGSTS: no registers held while in flight)
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+                 : "memory");
 }
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
-// spin until flags[i] reaches epoch (one thread; the caller's barrier publishes it to the CTA)
-__device__ __forceinline__ void wait_flag(const int* flags, int i, int epoch) {
-    while (ld_acquire_gpu(flags + i) < epoch) __nanosleep(64);
-}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 inline bool pdl_enabled() {
     static const bool on = [] {
@@ -114,6 +108,12 @@ struct Rec {
     static constexpr int HG = HE + R;
     static constexpr int REC = HG + R * C;
     static constexpr int RS = (2 * R - 1) + C;
+    // back-substitution row with the spike toward the left super-separator
+    static constexpr int RSM = RS + R;
+    // affine map of one inner separator of a KA tile: component q, basis b in
+    // [value (C) | left super-separator zL (R) | right super-separator zR (R)]
+    static constexpr int NB = C + 2 * R;
+    static constexpr int MAPF = R * NB;
 };
 
 __host__ __device__ constexpr int rows_per_chunk(int R, int C) { return tile_rows_per_chunk(R, C); }
@@ -124,48 +124,17 @@ __device__ __forceinline__ constexpr int offi(int i, int j, int R) { return i * 
 // that are dead for a given unrolled iteration must still be in bounds
 __host__ __device__ constexpr int cl(int x, int n) { return x < 0 ? 0 : (x >= n ? n - 1 : x); }
 
-// Paired FP32 (sm_100 FFMA2 / FMUL2): two independent elements of a register
-// row per instruction, each rounded exactly like fmaf / __fmul_rn (results are
-// bit-identical to the scalar loop); a scalar operand is a native broadcast
-// (R.F32).  FFMA2 has the FFMA pipe throughput but half the issue slots
-// (scripts/micro/ffma2.cu on B200: 36.7 vs 36.2 T FMA/s alone, 27.3 vs 20.6
-// interleaved with IMADs).  Inside one elimination chain, though, the pairs do
-// not survive the window shifts: ptxas adds moves and spills that cancel the
-// saving (measured -1..+1 % on c2-c5), so SGWLS_FFMA2 defaults to 0.
-#ifndef SGWLS_FFMA2
-#define SGWLS_FFMA2 0
-#endif
 // dst[k] = fma(s, src[k], dst[k]), k < N
 template <int N>
 __device__ __forceinline__ void row_fma(float* dst, float s, const float* src) {
 #pragma unroll
-    for (int k = 0; k + 1 < N; k += 2) {
-#if SGWLS_FFMA2
-        const float2 r = __ffma2_rn(make_float2(src[k], src[k + 1]), make_float2(s, s), make_float2(dst[k], dst[k + 1]));
-        dst[k] = r.x;
-        dst[k + 1] = r.y;
-#else
-        dst[k] = fmaf(s, src[k], dst[k]);
-        dst[k + 1] = fmaf(s, src[k + 1], dst[k + 1]);
-#endif
-    }
-    if (N & 1) dst[N - 1] = fmaf(s, src[N - 1], dst[N - 1]);
+    for (int k = 0; k < N; ++k) dst[k] = fmaf(s, src[k], dst[k]);
 }
 // dst[k] = src[k] * s, k < N
 template <int N>
 __device__ __forceinline__ void row_mul(float* dst, const float* src, float s) {
 #pragma unroll
-    for (int k = 0; k + 1 < N; k += 2) {
-#if SGWLS_FFMA2
-        const float2 r = __fmul2_rn(make_float2(src[k], src[k + 1]), make_float2(s, s));
-        dst[k] = r.x;
-        dst[k + 1] = r.y;
-#else
-        dst[k] = src[k] * s;
-        dst[k + 1] = src[k + 1] * s;
-#endif
-    }
-    if (N & 1) dst[N - 1] = src[N - 1] * s;
+    for (int k = 0; k < N; ++k) dst[k] = src[k] * s;
 }
 
 // squared 2-D distance of the edge (q - t, q), q at in-row index jj (regular band)
@@ -402,21 +371,15 @@ struct Win {
 
 // Spike-forward over one chunk: eliminates the interior, leaves sigma_j in
 // slots 0..R-1 (non-last chunk) and the head update of sigma_{j-1}; writes the
-// chunk record into `rec` (stride `rs` floats between fields).
+// chunk record into `rec` (shared memory, stride `rs` floats between fields).
 // FULL: the chunk has all RW rows (every chunk but possibly the band's last):
 // the position loop is then free of runtime predicates, so the window shifts
 // compile to register renames.
 template <int R, int C, int CG, int RW, bool FULL>
 __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                         bool last, int kv, float* rec, int rs, float* grec,
-                                                         int gs) {
+                                                         bool last, int kv, float* rec, int rs) {
     using RL = Rec<R, C>;
-    // every record field goes to `rec` (shared) and to `grec` (global; 32-bit field
-    // stride, so each field address is one IMAD.WIDE)
-    auto put = [&](int f, float v) {
-        rec[f * rs] = v;
-        grec[f * gs] = v;
-    };
+    auto put = [&](int f, float v) { rec[f * rs] = v; };
     constexpr int K = RW * (2 * R + 1);
     Win<R, C, true> w;
     w.clear();
@@ -473,11 +436,11 @@ __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG,
 
 template <int R, int C, int CG, int RW>
 __device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                    bool last, int kv, float* rec, int rs, float* grec, int gs) {
+                                                    bool last, int kv, float* rec, int rs) {
     if (kv == RW * (2 * R + 1))
-        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs, grec, gs);
+        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs);
     else
-        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lam, has_left, last, kv, rec, rs, grec, gs);
+        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lam, has_left, last, kv, rec, rs);
 }
 
 // ---------------------------------------------- block window (separator level)
@@ -562,6 +525,10 @@ struct BWin {
             for (int i = mm + 1; i < W2; ++i) bs[(i - mm - 1) * bstride] = cc[i];
 #pragma unroll
             for (int c = 0; c < C; ++c) bs[(W2 - 1 + c) * bstride] = g[mm][c] * inv;
+            if (SPIKE) {  // x_mm also depends on the left super-separator: + (Q/pivot) . zL
+#pragma unroll
+                for (int q = 0; q < R; ++q) bs[(W2 - 1 + C + q) * bstride] = Q[mm][q] * inv;
+            }
         }
     }
     __device__ __forceinline__ void shift() {
@@ -691,6 +658,108 @@ __device__ __forceinline__ void reduce_super(const float* recs, long long rs, lo
 }
 
 
+// KA's in-tile reduction with affine separator maps.  The forward sweep is
+// reduce_super's (the chunk records of one band in shared memory -> the
+// super-record), keeping each elimination's back-substitution row, spike to
+// the left super-separator included (bsm: row (s, mm) field f at
+// bsm[((s*R + mm)*RSM + f)*32]).  The backward sweep then runs SYMBOLICALLY
+// in the two unknown super-separators (maps_backward_column, one basis column
+// per warp): every inner separator s of the tile (s < nw - 1) comes out as
+// x_s = a_s + B_s zL + Cm_s zR, stored at maps[(s*MAPF + q*NB + b)*ms]
+// (b: value | zL | zR basis).  Once K2 has solved the super-separators, any
+// chunk separator is 2R^2 + R FMAs away -- no third solve over the chunk
+// records (the former KC launch) and no record round trip through HBM.
+template <int R, int C>
+__device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int nw, bool first_super,
+                                                 bool last_super, float* out, long long os, float* bsm) {
+    using RL = Rec<R, C>;
+    constexpr int RSM = RL::RSM;
+    auto bsrow = [&](int s, int mm) { return bsm + (s * R + mm) * RSM * 32; };
+    BWin<R, C, true> w;
+    w.clear_all();
+    if (!first_super) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            w.he[q] = recs[(RL::HE + q) * rs];
+#pragma unroll
+            for (int c = 0; c < C; ++c) w.hg[q][c] = recs[(RL::HG + q * C + c) * rs];
+#pragma unroll
+            for (int q2 = q + 1; q2 < R; ++q2) w.hoff[q][q2] = recs[(RL::HOFF + offi(q, q2, R)) * rs];
+        }
+    }
+    const int nblk = last_super ? nw - 1 : nw;
+    for (int s = 0; s < nblk; ++s) {
+        const float* t = recs + s * 32;
+        const float* h = recs + (s + 1) * 32;
+        enter_block<R, C, true>(w, t, h, rs, s < nw - 1, s > 0, s > 0 || !first_super);
+        if (s > 0) {
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, bsrow(s - 1, mm), 32);
+        }
+        w.shift();
+    }
+    if (last_super) {
+        if (nblk > 0) {
+            w.clear_hi();
+#pragma unroll
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, bsrow(nblk - 1, mm), 32);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+#pragma unroll
+            for (int k2 = i + 1; k2 < R; ++k2) out[(RL::TOFF + offi(i, k2, R)) * os] = w.A[i][k2];
+#pragma unroll
+            for (int q = 0; q < R; ++q) out[(RL::TCROSS + i * R + q) * os] = w.Q[i][q];
+            out[(RL::TE + i) * os] = w.e[i];
+#pragma unroll
+            for (int c = 0; c < C; ++c) out[(RL::TG + i * C + c) * os] = w.g[i][c];
+        }
+    }
+    if (!first_super) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+#pragma unroll
+            for (int q2 = q + 1; q2 < R; ++q2) out[(RL::HOFF + offi(q, q2, R)) * os] = w.hoff[q][q2];
+            out[(RL::HE + q) * os] = w.he[q];
+#pragma unroll
+            for (int c = 0; c < C; ++c) out[(RL::HG + q * C + c) * os] = w.hg[q][c];
+        }
+    }
+}
+
+// Symbolic back substitution of one basis column b of the maps (value channel,
+// zL component or zR component): the columns are independent, so the warps of
+// the KA tile share them.  x_{nw-1} is the right super-separator itself.
+template <int R, int C>
+__device__ __forceinline__ void maps_backward_column(const float* bsm, int nw, bool last_super, int b, float* maps,
+                                                     long long ms) {
+    using RL = Rec<R, C>;
+    constexpr int NB = RL::NB, RSM = RL::RSM;
+    float xn[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) xn[q] = (!last_super && b == C + R + q) ? 1.f : 0.f;
+    const int boff = b < C ? 2 * R - 1 + b : (b < C + R ? 2 * R - 1 + b : -1);  // value / spike field, zR: none
+    for (int s = nw - 2; s >= 0; --s) {
+        float xc[R];
+#pragma unroll
+        for (int mm = R - 1; mm >= 0; --mm) {
+            const float* o = bsm + (s * R + mm) * RSM * 32;
+            float v = boff >= 0 ? o[boff * 32] : 0.f;
+#pragma unroll
+            for (int i = mm + 1; i < 2 * R; ++i)
+                v = fmaf(o[(i - mm - 1) * 32], (i < R) ? xc[i < R ? i : 0] : xn[i >= R ? i - R : 0], v);
+            xc[mm] = v;
+        }
+        float* mo = maps + ((long long)s * RL::MAPF + b) * ms;
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+            mo[(long long)q * NB * ms] = xc[q];
+            xn[q] = xc[q];
+        }
+    }
+}
+
 // Solve the inner separators of a run of `nw` chunk records (inner separators =
 // the separators of chunks 0..nw-2) with the left / right separators known
 // (has_l: zL, has_r: zR).  Record s's field f is at recs[s*cs + f*rs]; the
@@ -782,12 +851,8 @@ __device__ __forceinline__ void solve_inner(const float* recs, long long rs, lon
 // system (level 2), then every warp solves its group's inner super-separators
 // with the two group separators as boundary values (level 3, in parallel).
 // Sequential depth ~ 2*PS/NG + NG instead of 2*PS.
-// Body of the tree solve for one group of 32 lines (lane = line, w = warp),
-// usable both as its own kernel and from the last KA tile of a band group.
+// Body of the tree solve for one group of 32 lines (lane = line, w = warp).
 template <int R, int C>
-// `rec` is deliberately not __restrict__: in the fused form the records were
-// written by other CTAs of the same launch, so they must not be read through
-// the non-coherent (LDG.CONSTANT) path.
 __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec,
                                              float* __restrict__ rsc, float* __restrict__ z, float* sm, int lane,
                                              int w, int NG, int group) {
@@ -864,45 +929,30 @@ template <int R, int C, int CG>
 #define SGWLS_KA_MINB (R >= 2 ? 4 : 3)
 #endif
 #define SGWLS_KA_BOUNDS __launch_bounds__(256, SGWLS_KA_MINB)
-#ifndef SGWLS_KB_MINB_KC
-// KB after KC: <= 85 registers (measured +3% c5, +8% c4); <= 64 for one channel
+#ifndef SGWLS_KB_MINB
+// KB: <= 85 registers (measured +3% c5, +8% c4); <= 64 for one channel
 // once the averaging went to shuffles and direct stores (c5 +1.6 %, c3 +0.7 %; c4 -1 %)
-#define SGWLS_KB_MINB_KC (C == 1 ? 4 : 3)
+#define SGWLS_KB_MINB (C == 1 ? 4 : 3)
 #endif
-// the INNER variant (r = 1) spills badly under a tighter budget: 2 CTAs (<= 128)
-#ifndef SGWLS_KB_MINB_INNER
-// the r = 1 INNER KB: <= 85 registers for one channel (c1 +2.3 %), <= 128 with
-// several (3 CTAs spill: c2 -16 %)
-#define SGWLS_KB_MINB_INNER (C == 1 ? 3 : 2)
-#endif
-#define SGWLS_KB_BOUNDS __launch_bounds__(256, (INNER ? SGWLS_KB_MINB_INNER : SGWLS_KB_MINB_KC))
+#define SGWLS_KB_BOUNDS __launch_bounds__(256, SGWLS_KB_MINB)
 __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
-                                               float* __restrict__ rsc, float* __restrict__ zs,
-                                               int* __restrict__ counters, float* __restrict__ crec,
-                                               const __grid_constant__ WeightDev W, int* __restrict__ flags,
-                                               int epoch, int opts) {
+                                               float* __restrict__ maps, const __grid_constant__ WeightDev W) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1;
     using RL = Rec<R, C>;
     extern __shared__ float sm[];
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
     const int NL = g.nb * g.batch;
-    // grid: (line group, tile) or, with jfast, (tile, line group): the tiles of
-    // one group are then dispatched together and groups complete in order
-    // opts bit 0: jfast grid order; bit 1: trigger the dependent launch only
-    // after this tile's chunks are done (KB's prologue then overlaps the tail
-    // and the reduced solves instead of competing with the chunk work)
-    const bool jfast = opts & 1, late = (opts >> 1) & 1;
-    const int grp = jfast ? blockIdx.y : blockIdx.x;
-    const int L = grp * 32 + lane;
-    const int J = jfast ? blockIdx.x : blockIdx.y;
+    // grid: (line group, tile)
+    const int L = blockIdx.x * 32 + lane;
+    const int J = blockIdx.y;
     const int j = J * NW + wid;
     const int nw = min(NW, g.P - J * NW);
     const int rs = NW * 32 + 1;  // smem record field stride
     float* rec = sm + wid * 32 + lane;
     pdl_wait();  // the pass input is the previous pass's output
-    if (!late) pdl_trigger();
+    pdl_trigger();
     if (L < NL && wid < nw) {
         const int img = g.batch == 1 ? 0 : L / g.nb, b = L - img * g.nb;  // no integer division for one image
         const int lo = band_lo(g, b);
@@ -911,43 +961,29 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
         ChunkIn<R, C, CG, RW> in;
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows,
                                  nullptr, L);
-        // every chunk record also goes to HBM for KC / KB (nothing downstream redoes the spike-forward)
-        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0 || g.has_prev, j == g.P - 1 && !g.has_next, nrows * M, rec, rs,
-                                          crec + (long long)j * RL::REC * NL + L, NL);
+        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0 || g.has_prev, j == g.P - 1 && !g.has_next, nrows * M, rec,
+                                          rs);
     }
     __syncthreads();
-    if (late) pdl_trigger();
-    const int PS = jfast ? gridDim.x : gridDim.y;  // = ceil(P / NW), the grid's tile dimension
-    if (wid == 0 && L < NL) {
-        const long long NLl = NL;
-        reduce_super<R, C>(sm + lane, rs, 32, nw, J == 0 && !g.has_prev, J == PS - 1 && !g.has_next,
-                           srec + (long long)J * RL::REC * NLl + L, NLl);
-    }
-    if (counters == nullptr) return;
-    // ---- the last tile of this band group to finish solves the group's
-    //      reduced system (K2) right here: no separate launch, and the solve
-    //      overlaps the remaining tiles of other groups.
-    __shared__ int s_last;
-    __threadfence();  // publish this tile's super-records before counting it
+    const int PS = gridDim.y;  // = ceil(P / NW), the grid's tile dimension
+    const long long NLl = NL;
+    float* bsm = sm + RL::REC * rs + lane;
+    const bool last_super = J == PS - 1 && !g.has_next;
+    if (wid == 0 && L < NL)  // super-record for K2, back-substitution rows
+        reduce_super_fwd<R, C>(sm + lane, rs, nw, J == 0 && !g.has_prev, last_super,
+                               srec + (long long)J * RL::REC * NLl + L, NLl, bsm);
+    if (nw < 2) return;
     __syncthreads();
-    if (wid == 0 && lane == 0) {
-        const int done = atomicAdd(&counters[grp], 1);
-        s_last = (done == PS - 1);
-        if (s_last) counters[grp] = 0;  // ready for the next pass / replay
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    PassGeom gs = g;
-    gs.P = PS;
-    k2_tree_body<R, C>(gs, srec, rsc, zs, sm, lane, wid, NW, grp);
-    if (flags != nullptr) {  // publish: this group's super-separators (and every record) are final
-        __syncthreads();
-        if (wid == 0 && lane == 0) {
-            __threadfence();
-            st_release_gpu(&flags[grp], epoch);
-        }
-    }
+    // the affine maps of the tile's inner separators for KB, one basis column per warp
+    if (L < NL)
+        for (int b = wid; b < RL::NB; b += NW)
+            maps_backward_column<R, C>(bsm, nw, last_super, b, maps + (long long)J * NW * RL::MAPF * NLl + L, NLl);
+}
+
+template <int R, int C>
+__host__ inline size_t ka_smem(int NWA) {
+    using RL = Rec<R, C>;
+    return ((size_t)RL::REC * (NWA * 32 + 1) + (size_t)(NWA > 1 ? NWA - 1 : 1) * R * RL::RSM * 32) * sizeof(float);
 }
 
 // Interior solve of one chunk with both separators known (zl: previous
@@ -1147,11 +1183,9 @@ struct TileOut {
     int transpose_out;
     int step;       // CTA band stride (32 - halo)
     int nph;        // accumulation phases
-    int early_rec;  // INNER: the predecessor is a separate K2 launch (records complete before it triggers)
-    int rowmaj_odd; // row-major output tile also for odd tau (one channel, short columns)
-    const int* flags;  // ready-flag mode (INNER): per-band-group flags raised by KA, else nullptr
-    int epoch;         // flag value of this pass
-    int jfast;         // grid order (chunk tile fastest)
+    int nwa;        // chunks per KA tile (the tiles KA's separator maps refer to)
+    int psa;        // KA tiles per band
+    int early;      // the predecessor is a K2 launch (it waited for KA): KA's maps may be read before the wait
 };
 
 // 1/n correctly rounded (what 1.0f / n gives) for the band count of a column, n <= 2r + 2 <= 10
@@ -1170,63 +1204,6 @@ __device__ __forceinline__ void covering(const PassGeom& g, int x, int& bmin, in
         if (b1 < b0) bmin = g.nreg;
         bmax = g.nreg;
     }
-}
-
-// ===================================================================== KC
-//
-// Every chunk separator from the super-separators: thread (tile J, line L)
-// solves the tile's inner separators with the two known super-separators as
-// boundary values from KA's chunk records (lane per line, fully parallel over
-// tiles), and writes all separators of the tile's chunks to `sep`
-// ([chunk][q][c][line]).  KB then solves every chunk interior independently.
-#ifndef SGWLS_KC_MINB
-#define SGWLS_KC_MINB 1
-#endif
-template <int R, int C>
-__global__ void __launch_bounds__(128, SGWLS_KC_MINB) kc_inner(const PassGeom g, int NWA, int PSA, const float* __restrict__ crec,
-                                                const float* __restrict__ zs, float* __restrict__ sep) {
-    using RL = Rec<R, C>;
-    extern __shared__ float sm[];
-    const int lane = threadIdx.x, ty = threadIdx.y, NTY = blockDim.y;
-    const int tid = ty * 32 + lane, NT = NTY * 32;
-    const int NL = g.nb * g.batch;
-    const long long NLl = NL;
-    const int L = blockIdx.x * 32 + lane;
-    const int J = blockIdx.y * NTY + ty;
-    pdl_wait();  // K2's super-separators (and, through K2, KA's records)
-    pdl_trigger();
-    if (L >= NL || J >= PSA) return;
-    const int nw = min(NWA, g.P - J * NWA);
-    const bool has_l = J > 0 || g.has_prev, has_r = J < PSA - 1 || g.has_next;
-    float zL[R][C], zR[R][C];
-#pragma unroll
-    for (int q = 0; q < R; ++q)
-#pragma unroll
-        for (int c = 0; c < C; ++c) {
-            zL[q][c] = has_l ? zs[((long long)(J - 1) * R * C + q * C + c) * NLl + L] : 0.f;
-            zR[q][c] = has_r ? zs[((long long)J * R * C + q * C + c) * NLl + L] : 0.f;
-        }
-    float* out = sep + (long long)J * NWA * R * C * NLl + L;
-    if (J == 0 && g.has_prev) {  // slab mode: the previous slab's separator, for the first chunk's KB
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-#pragma unroll
-            for (int c = 0; c < C; ++c) out[((long long)(-R + q) * C + c) * NLl] = zL[q][c];
-    }
-    if (has_r) {  // the tile's last separator is the super-separator (stored before the solve, see KB note)
-#pragma unroll
-        for (int q = 0; q < R; ++q)
-#pragma unroll
-            for (int c = 0; c < C; ++c) out[((long long)((nw - 1) * R + q) * C + c) * NLl] = zR[q][c];
-    }
-    solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(crec + (long long)J * NWA * RL::REC * NLl + L, NLl, (long long)RL::REC * NLl, nw, has_l, zL,
-                      has_r, zR, out, NLl, sm + tid, NT);
-}
-
-template <int R, int C>
-__host__ inline size_t kc_smem(int NWA, int nty) {
-    using RL = Rec<R, C>;
-    return (size_t)(NWA > 1 ? NWA - 1 : 1) * R * RL::RS * 32 * nty * sizeof(float);
 }
 
 // ============================================================ row-slab mode
@@ -1359,29 +1336,53 @@ __host__ inline size_t k2_slab_solve_smem(int NG) {
 
 // ===================================================================== KB
 
-// Two ways to get a chunk's separators:
-//   INNER = false: from `zsep` = every chunk separator, written by KC;
-//   INNER = true : KB tiles coincide with KA tiles; the tile loads its chunk
-//                  records (`crec`) into shared memory and warp 0 solves the
-//                  inner separators from the two super-separators `zsep` = zs
-//                  (one launch fewer per pass: better for small images).
-template <int R, int C, int CG, bool INNER>
+// A chunk's two separators come from KA's affine maps of its KA tile's inner
+// separators and the super-separators K2 solved (zsep; the first chunk of a
+// row slab reads the previous slab's separator at zsep[-1]).  Chunk j lies in
+// KA tile JA = j / nwa at s = j % nwa: its right separator sigma_j is inner
+// (a map of the tile's zA = zsep[JA-1], zB = zsep[JA]) or zB itself; its left
+// separator sigma_{j-1} is inner in the same tile (s > 0) or zA -- so the two
+// super-separators zA, zB are all a chunk reads from K2.
+__device__ __forceinline__ bool inner_separator(const PassGeom& g, const TileOut& to, int js) {
+    if (js < 0) return false;
+    const int JA = js / to.nwa;
+    return js - JA * to.nwa < to.nwa - 1 && js < g.P - 1;
+}
+
+// x = a + B zA + Cm zB from a map staged in shared memory (fields at ms[f*32])
+template <int R, int C>
+__device__ __forceinline__ void apply_map(const float* ms, const float (&zA)[R][C], const float (&zB)[R][C],
+                                          float (&z)[R][C]) {
+    constexpr int NB = Rec<R, C>::NB;
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            float v = ms[(q * NB + c) * 32];
+#pragma unroll
+            for (int p = 0; p < R; ++p) v = fmaf(ms[(q * NB + C + p) * 32], zA[p][c], v);
+#pragma unroll
+            for (int p = 0; p < R; ++p) v = fmaf(ms[(q * NB + C + R + p) * 32], zB[p][c], v);
+            z[q][c] = v;
+        }
+}
+
+template <int R, int C, int CG>
 __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, const float* __restrict__ zsep,
-                                               const float* __restrict__ crec, const TileOut to,
+                                               const float* __restrict__ maps, const TileOut to,
                                                unsigned long long* __restrict__ err,
                                                const __grid_constant__ WeightDev W) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1, K = RW * M;
-    using RL = Rec<R, C>;
     extern __shared__ float sm[];
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
     const int tid = wid * 32 + lane, NT = NW * 32;
-    // grid: (band tile, chunk tile, image) or, with jfast, (chunk tile, band tile, image)
-    const int bxi = to.jfast ? blockIdx.y : blockIdx.x;
+    // grid: (band tile, chunk tile, image)
+    const int bxi = blockIdx.x;
     const int B0 = bxi * to.step;
     const int b = B0 + lane;
-    const int J = to.jfast ? blockIdx.x : blockIdx.y;
+    const int J = blockIdx.y;
     const int img = blockIdx.z;
     const int j = J * NW + wid;
     const int nw = min(NW, g.P - J * NW);
@@ -1392,13 +1393,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int Y0 = J * NW * RW;
     const int TR = min(NW * RW, g.Hl - Y0);  // tile rows
 
-    // smem: INNER: [recs | zint | bsc] then the output tile; else the tile only
-    const int rs = NT + 1;
-    float* recs = sm;                                    // REC x rs
-    float* zint = recs + RL::REC * rs;                   // NW x R*C x 32
-    float* bsc = zint + NW * R * C * 32;                 // (NW) x R x RS x 32 back-substitution rows
-    const int region1 = INNER ? (RL::REC * rs + NW * R * C * 32 + (NW * R * RL::RS + R * C) * 32 + 3) & ~3 : 0;
-    float* tl = sm + region1;                            // output tile [x][y*C + c]
+    float* tl = sm;  // output tile [x][y*C + c] or [y][x*C + c]
     const int bl = min(B0 + 32, g.nb) - 1;
     const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
     const int ncol = xb - xa + 1;
@@ -1414,40 +1409,26 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     // mod 8) and 8-way for even tau; row-major with an odd pitch is conflict-free
     // (odd tau) or 2-way (even tau) for one channel, and its columns still leave
     // as float4 stores (4 gathered rows).  Bulk copies need column-major.
-    const bool colmaj = to.transpose_out && vec && (n >= 64 || C > 1 || ((g.tau & 1) && !to.rowmaj_odd));
+    const bool colmaj = to.transpose_out && vec && (n >= 64 || C > 1);
     const int TP = ((n + 3) & ~3) + ((((n + 3) & ~3) % 8 == 0) ? 4 : 8);
     const int XP = (ncol * C) | 1;
     const int sx = colmaj ? TP : C, sy = colmaj ? C : XP;  // tile strides of x and y
     const int tsize = colmaj ? ncol * TP : TR * XP;
 
-    // ---- 1. chunk inputs and edge weights, before the wait when separators
-    //         come from a predecessor (KA finished with the pass input before
-    //         K2/KC trigger); single-chunk lines wait first.
+    // ---- 1. chunk inputs and edge weights before the dependent-launch wait:
+    //         the pass input was complete before KA began
     ChunkIn<R, C, CG, RW> in;
     const int y0 = j * RW;
     const int nrows = active ? min(RW, g.Hl - y0) : 0;
     const int lo = active ? band_lo(g, b) : 0;
-    // KA's records may be read before the wait only when the predecessor is a
-    // K2/KC launch (those trigger after waiting for KA); after a fused or
-    // absent K2 the predecessor is KA itself.
     const bool multi = g.P > 1 || g.has_prev || g.has_next;  // separators exist
-    // ready-flag mode: KA runs the reduced solve per band group and raises a
-    // flag; this tile waits for the (at most two) groups its bands belong to.
-    // Records and separators are then read through L2 (ld.cg: written by a
-    // grid that may still be running).
-    const bool flagged = INNER && multi && to.flags != nullptr;
-    const bool early = flagged || (multi && (!INNER || to.early_rec));
     // ---- 0. tile geometry (column ownership, 1/count, zeroing): independent of the
     //         predecessor, so it runs before the dependent-launch wait
     // Shuffle averaging (average_shfl) when the bands overlap, all bands of the
     // tile are on the tau grid, tau <= 3, and the last owned column has a writer lane
     const bool last_cta = B0 + 32 >= g.nb;
-#ifndef SGWLS_NO_SHFL_AVG
     const bool shfl_avg = to.nph > 1 && g.tau <= 3 && bl < g.nreg &&
                           (!last_cta || (bl - B0) + div_tau(g, M - 1) <= 31);
-#else
-    const bool shfl_avg = false;
-#endif
     // per-column averaging scale 1/count, positive if this CTA owns the column
     // (writes it out), negative otherwise
     float* inv_col = tl + ((tsize + 3) & ~3);
@@ -1459,7 +1440,6 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         const bool owned = bx == 0 ? q <= 0 : (q > (bx - 1) * to.step && q <= bx * to.step);
         const float inv = kInvCount[bmax - bmin + 1];  // == 1.0f / count, without the IEEE-division slow path
         inv_col[xl] = owned ? inv : -inv;
-#ifndef SGWLS_ZERO_ALL
         if (to.nph == 2 && !shfl_avg) {
             // phase 0 STORES (step 4), so only the columns no phase-0 band of this
             // tile covers start from zero (measured: c5 +1.2 %, c4 +0.7 %; with
@@ -1474,36 +1454,43 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
 #pragma unroll
                     for (int c = 0; c < C; ++c) tl[xl * sx + y * sy + c] = 0.f;
         }
-#endif
     }
-#ifdef SGWLS_ZERO_ALL  // A/B: zero the whole tile, every phase accumulates
-    const bool store_first = false;
-#else
     const bool store_first = to.nph == 2;
-#endif
     if (to.nph > 1 && !store_first && !shfl_avg) {
         for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    if (!early) pdl_wait();
+    // this chunk's separator maps -> shared memory (per warp: slot 0 = sigma_{j-1},
+    // slot 1 = sigma_j), asynchronously; before the wait when KA is not the predecessor
+    using RL = Rec<R, C>;
+    float* mapsm = inv_col + ((ncol + 3) & ~3) + wid * 2 * RL::MAPF * 32 + lane;
+    const int JA = j / to.nwa, sj = j - JA * to.nwa;
+    const bool lastc = (j == g.P - 1) && !g.has_next;
+    const bool has_left = j > 0 || g.has_prev;
+    const bool r_inner = !lastc && inner_separator(g, to, j);
+    const bool l_inner = sj > 0;  // sigma_{j-1} inner in the same KA tile
+    auto fetch_maps = [&]() {
+        if (!(active && multi)) return;
+        const float* gp = maps + (long long)j * RL::MAPF * NLl + L;
+        if (l_inner) {
+#pragma unroll
+            for (int f = 0; f < RL::MAPF; ++f) cp_async4(mapsm + f * 32, gp - (RL::MAPF - f) * NLl);
+        }
+        if (r_inner) {
+#pragma unroll
+            for (int f = 0; f < RL::MAPF; ++f) cp_async4(mapsm + (RL::MAPF + f) * 32, gp + f * NLl);
+        }
+        cp_async_commit();
+    };
+    if (to.early) fetch_maps();
     if (active)
         load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
                                  L);
-    if (flagged) {
-        if (tid == 0) {
-            const int lfirst = img * g.nb + B0, llast = img * g.nb + min(B0 + 31, g.nb - 1);
-            wait_flag(to.flags, lfirst >> 5, to.epoch);
-            if ((llast >> 5) != (lfirst >> 5)) wait_flag(to.flags, llast >> 5, to.epoch);
-        }
-        __syncthreads();
-    }
-    if (INNER && multi && active) {  // KA's record of this chunk
-        const float* srcr = crec + (long long)j * RL::REC * NLl + L;
-#pragma unroll
-        for (int f = 0; f < RL::REC; ++f) recs[f * rs + tid] = __ldcg(srcr + (long long)f * NLl);
-    }
-    if (early && !flagged) pdl_wait();  // separators
+    pdl_wait();  // super-separators (K2), maps (KA)
     pdl_trigger();
+    if (!to.early) fetch_maps();
 
+    // ---- 2. this chunk's two separators: the KA tile's super-separators zA
+    //         (left, zsep[JA-1]) and zB (right, zsep[JA]) from K2, the maps
     float zl[R][C], zr[R][C];
 #pragma unroll
     for (int q = 0; q < R; ++q)
@@ -1512,61 +1499,33 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             zl[q][c] = 0.f;
             zr[q][c] = 0.f;
         }
-    const bool lastc = (j == g.P - 1) && !g.has_next;
-    const bool has_left = j > 0 || g.has_prev;
-    if constexpr (INNER) {
-        const int PS = to.jfast ? gridDim.x : gridDim.y;  // = ceil(P / NW)
-        __syncthreads();
-        // ---- 2. lane-per-band solve of the tile's inner separators with the
-        //         two known super-separators as boundary values
-        if (wid == 0 && b < g.nb && multi) {
-            const bool has_l = J > 0 || g.has_prev, has_r = J < PS - 1 || g.has_next;
-            float zL[R][C], zR[R][C];
+    if (active && multi) {
+        const bool hA = JA > 0 || g.has_prev, hB = JA < to.psa - 1 || g.has_next;
+        const float* zb = zsep + (long long)JA * R * C * NLl + L;
+        float zA[R][C], zB[R][C];
 #pragma unroll
-            for (int q = 0; q < R; ++q)
+        for (int q = 0; q < R; ++q)
 #pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    zL[q][c] = has_l ? __ldcg(zsep + ((long long)(J - 1) * R * C + q * C + c) * NLl + L) : 0.f;
-                    zR[q][c] = has_r ? __ldcg(zsep + ((long long)J * R * C + q * C + c) * NLl + L) : 0.f;
-                }
-            // The boundary values are stored BEFORE the solve: nvcc 12.9 was seen to
-            // reuse the register holding `nw` as the back-substitution loop counter
-            // and then address `zint[nw - 1]` with the decremented value.
-            if (has_r) {
-#pragma unroll
-                for (int q = 0; q < R; ++q)
-#pragma unroll
-                    for (int c = 0; c < C; ++c) zint[(((nw - 1) * R + q) * C + c) * 32 + lane] = zR[q][c];
+            for (int c = 0; c < C; ++c) {
+                zA[q][c] = hA ? zb[((long long)(q - R) * C + c) * NLl] : 0.f;
+                zB[q][c] = hB ? zb[(q * C + c) * NLl] : 0.f;
             }
-            // publish the left super-separator for the tile's first chunk (slot after the bs rows)
+        cp_async_wait_all();  // this lane's own map columns (no cross-lane reads: no warp barrier)
+        if (r_inner) {
+            apply_map<R, C>(mapsm + RL::MAPF * 32, zA, zB, zr);
+        } else if (!lastc) {
 #pragma unroll
             for (int q = 0; q < R; ++q)
 #pragma unroll
-                for (int c = 0; c < C; ++c) bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane] = zL[q][c];
-            solve_inner<R, C>(recs + lane, rs, 32, nw, has_l, zL, has_r, zR, zint + lane, 32, bsc + lane, 32);
+                for (int c = 0; c < C; ++c) zr[q][c] = zB[q][c];
         }
-        __syncthreads();
-        if (active && multi) {
+        if (l_inner) {
+            apply_map<R, C>(mapsm, zA, zB, zl);
+        } else if (has_left) {
 #pragma unroll
             for (int q = 0; q < R; ++q)
 #pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    if (has_left)
-                        zl[q][c] = (wid == 0) ? bsc[((long long)(NW * R * RL::RS) + q * C + c) * 32 + lane]
-                                              : zint[(((wid - 1) * R + q) * C + c) * 32 + lane];
-                    if (!lastc) zr[q][c] = zint[((wid * R + q) * C + c) * 32 + lane];
-                }
-        }
-    } else {
-        // ---- 2. this chunk's two separators (KC)
-        if (active && multi) {
-#pragma unroll
-            for (int q = 0; q < R; ++q)
-#pragma unroll
-                for (int c = 0; c < C; ++c) {
-                    if (has_left) zl[q][c] = zsep[((long long)(j - 1) * R * C + q * C + c) * NLl + L];
-                    if (!lastc) zr[q][c] = zsep[((long long)j * R * C + q * C + c) * NLl + L];
-                }
+                for (int c = 0; c < C; ++c) zl[q][c] = zA[q][c];
         }
     }
     const int kv = nrows * M;
@@ -1615,7 +1574,6 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                 default: average_shfl_direct<3, R, C, K, DVEC>(ys, nrw, par0, lane, obase, opitch, ncol, inv_col); break;
             }
         }
-        if (flagged) pdl_wait();
         return;
     }
     if (shfl_avg) {
@@ -1726,21 +1684,15 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             }
         }
     }
-    // flag mode: this grid completes only after KA has (the next pass's KA waits on it)
-    if (flagged) pdl_wait();
 }
 
 // =========================================================== host helpers
 
 template <int R, int C>
-__host__ inline size_t kb_smem_bytes(bool inner, int NW, int TR, int ncol) {
-    using RL = Rec<R, C>;
-    const size_t NT = (size_t)NW * 32;
-    const size_t r1 = inner ? (((size_t)RL::REC * (NT + 1) + NW * R * C * 32 + ((size_t)NW * R * RL::RS + R * C) * 32 + 3) &
-                               ~(size_t)3)
-                            : 0;
+__host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
     const int n4 = (TR * C + 3) & ~3;
-    return (r1 + (size_t)ncol * (n4 + (n4 % 8 == 0 ? 4 : 8)) + ncol) * sizeof(float);
+    const size_t tile = (size_t)ncol * (n4 + (n4 % 8 == 0 ? 4 : 8));
+    return (((tile + 3) & ~(size_t)3) + ((ncol + 3) & ~3) + (size_t)NW * 2 * Rec<R, C>::MAPF * 32) * sizeof(float);
 }
 
 
@@ -1751,23 +1703,23 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
     using RL = Rec<R, C>;
     const PassGeom& g = pl.geom;
     const int NL = g.nb * g.batch;
-    const bool kc = pl.kc != 0;            // separators from KC (else KB solves its tile's inner ones)
-    const int NWA = kc ? pl.nwa : pl.nw;   // KA super-chunk (chunks per KA tile)
-    const int NW = pl.nw;                  // KB tile height (chunks)
+    const int NWA = pl.nwa;  // KA super-chunk (chunks per KA tile)
+    const int NW = pl.nw;    // KB tile height (chunks)
     const int PSA = (g.P + NWA - 1) / NWA;
     const int PB = (g.P + NW - 1) / NW;
     cudaError_t e;
     const bool slab = pl.slab_phase != 0;
-    if (pl.slab_phase == 1) {  // row-slab phase A: KA + slab record
-        {
-            ProfScope ps("ka_tile", st);
-            const size_t smem = (size_t)RL::REC * (NWA * 32 + 1) * sizeof(float);
-            e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, NWA), smem, st, g, pl.src, pl.guid,
-                           pl.rec, pl.rs, pl.z, (int*)nullptr, pl.crec, *pl.w, (int*)nullptr, 0, 0);
-            if (e != cudaSuccess) return e;
-        }
+    const bool multi = g.P > 1 || slab;
+    if (pl.slab_phase != 2 && multi) {  // KA (ordinary pass, or row-slab phase A)
+        ProfScope ps("ka_tile", st);
+        const size_t smem = ka_smem<R, C>(NWA);
+        e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, NWA), smem, st, g, pl.src, pl.guid,
+                       pl.rec, pl.maps, *pl.w);
+        if (e != cudaSuccess) return e;
+    }
+    if (pl.slab_phase == 1) {  // row-slab phase A: this slab's record
         ProfScope ps("k2_slab_reduce", st);
         const size_t sm2 = k2_slab_reduce_smem<R, C>(kSlabWarps);
         e = cudaFuncSetAttribute(k2_slab_reduce<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
@@ -1777,7 +1729,7 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         return cudaGetLastError();
     }
-    if (pl.slab_phase == 2) {  // row-slab phase B: separators, then KC / KB below
+    if (pl.slab_phase == 2) {  // row-slab phase B: super-separators, then KB below
         ProfScope ps("k2_slab_solve", st);
         const size_t sm2 = k2_slab_solve_smem<R, C>(kSlabWarps);
         e = cudaFuncSetAttribute(k2_slab_solve<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
@@ -1786,92 +1738,38 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
                        pl.islab, (const float*)pl.slabrec, (const float*)pl.rec, (const float*)pl.grec, pl.zg, pl.bsg,
                        pl.rs, pl.z);
         if (e != cudaSuccess) return e;
-    }
-    if (g.P > 1 && !slab) {
-        const bool flagged = pl.flags != nullptr && !kc && PSA > 1;
-        const bool fuse = pl.counters != nullptr && (flagged || tile_fuse_k2(PSA));
-        {
-            ProfScope ps("ka_tile", st);
-            const size_t smem_ka = (size_t)RL::REC * (NWA * 32 + 1) * sizeof(float);
-            const size_t smem_k2 = fuse ? k2_tree_smem<R, C>(NWA) : 0;
-            const size_t smem = smem_ka > smem_k2 ? smem_ka : smem_k2;
-            e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            static const int jfast = [] {
-                const char* v = std::getenv("SGWLS_KA_JFAST");  // tuning knob: KA grid order
-                return v ? std::atoi(v) : 0;
-            }();
-            static const int ka_late = [] {
-                const char* v = std::getenv("SGWLS_KA_LATE");  // tuning knob: late dependent-launch trigger
-                return v ? std::atoi(v) : 1;
-            }();
-            const dim3 grid = jfast ? dim3(PSA, (NL + 31) / 32) : dim3((NL + 31) / 32, PSA);
-            e = launch_pdl(ka_tile<R, C, CG>, grid, dim3(32, NWA), smem, st, g, pl.src,
-                           pl.guid, pl.rec, pl.rs, pl.z, fuse ? pl.counters : nullptr, pl.crec, *pl.w,
-                           flagged ? pl.flags : nullptr, pl.epoch, jfast | ((flagged && ka_late) ? 2 : 0));
-            if (e != cudaSuccess) return e;
-        }
-        if (PSA > 1 && !fuse) {
-            ProfScope ps("k2_tree", st);
-            PassGeom gs = g;
-            gs.P = PSA;
-            static const int ng_env = [] {
-                const char* v = std::getenv("SGWLS_K2_NG");  // tuning knob: warps (groups) of the K2 tree
-                const int n = v ? std::atoi(v) : 0;
-                return n == 4 || n == 8 || n == 16 ? n : 0;
-            }();
-            // measured on B200: 16 warps from 16 super records on (c2 +3 %), 8 below (c1)
-            const int NG = ng_env ? ng_env : (PSA >= 16 ? 16 : 8);
-            const size_t sm2 = k2_tree_smem<R, C>(NG);
-            e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
-            if (e != cudaSuccess) return e;
-            e = launch_pdl(k2_tree<R, C>, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs,
-                           pl.z);
-            if (e != cudaSuccess) return e;
-        }
-    }
-    if (kc && (g.P > 1 || slab)) {
-        {
-            ProfScope ps("kc_inner", st);
-            const int nty = 4;
-            const size_t smc = kc_smem<R, C>(NWA, nty);
-            e = cudaFuncSetAttribute(kc_inner<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smc);
-            if (e != cudaSuccess) return e;
-            e = launch_pdl(kc_inner<R, C>, dim3((NL + 31) / 32, (PSA + nty - 1) / nty), dim3(32, nty), smc, st, g, NWA,
-                           PSA, (const float*)pl.crec, (const float*)pl.z, pl.sep);
-            if (e != cudaSuccess) return e;
-        }
+    } else if (g.P > 1 && PSA > 1) {  // K2: the reduced system over the super-separators
+        ProfScope ps("k2_tree", st);
+        PassGeom gs = g;
+        gs.P = PSA;
+        static const int ng_env = [] {
+            const char* v = std::getenv("SGWLS_K2_NG");  // schedule knob: warps (groups) of the K2 tree
+            const int n = v ? std::atoi(v) : 0;
+            return n == 4 || n == 8 || n == 16 ? n : 0;
+        }();
+        // measured on B200: 16 warps from 16 super records on (c2 +3 %), 8 below (c1)
+        const int NG = ng_env ? ng_env : (PSA >= 16 ? 16 : 8);
+        const size_t sm2 = k2_tree_smem<R, C>(NG);
+        e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(k2_tree<R, C>, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs,
+                       pl.z);
+        if (e != cudaSuccess) return e;
     }
     {
         ProfScope ps("kb_tile", st);
         constexpr int RW = rows_per_chunk(R, C);
         const int ncol = 31 * g.tau + 2 * g.r + 1;
-        const size_t smem = kb_smem_bytes<R, C>(!kc, NW, NW * RW, ncol);
-        const bool flagged = g.P > 1 && pl.flags != nullptr && !kc && PSA > 1;
-        const bool k2_separate =
-            slab || (g.P > 1 && PSA > 1 && !flagged && !(tile_fuse_k2(PSA) && pl.counters != nullptr));
-        static const int kb_jfast = [] {
-            const char* v = std::getenv("SGWLS_KB_JFAST");  // tuning knob: KB grid order
-            return v ? std::atoi(v) : 0;
-        }();
-        static const int rowmaj_odd = [] {
-            const char* v = std::getenv("SGWLS_ROWMAJ_ODD");  // tuning knob
-            return v ? std::atoi(v) : 1;
-        }();
-        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, k2_separate ? 1 : 0, rowmaj_odd,
-                   flagged ? pl.flags : nullptr, pl.epoch, kb_jfast};
-        const dim3 kgrid = kb_jfast ? dim3(PB, pl.ncta, g.batch) : dim3(pl.ncta, PB, g.batch);
-        if (kc) {
-            e = cudaFuncSetAttribute(kb_tile<R, C, CG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            e = launch_pdl(kb_tile<R, C, CG, false>, kgrid, dim3(32, NW), smem, st, g, pl.src,
-                           pl.guid, (const float*)pl.sep, (const float*)nullptr, to, pl.err, *pl.w);
-        } else {
-            e = cudaFuncSetAttribute(kb_tile<R, C, CG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            if (e != cudaSuccess) return e;
-            e = launch_pdl(kb_tile<R, C, CG, true>, kgrid, dim3(32, NW), smem, st, g, pl.src,
-                           pl.guid, (const float*)pl.z, (const float*)pl.crec, to, pl.err, *pl.w);
-        }
+        const size_t smem = kb_smem_bytes<R, C>(NW, NW * RW, ncol);
+        // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
+        // triggering) or, with a single KA tile per band, KA itself
+        const bool early = slab || PSA > 1;
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0};
+        const dim3 kgrid(pl.ncta, PB, g.batch);
+        e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = launch_pdl(kb_tile<R, C, CG>, kgrid, dim3(32, NW), smem, st, g, pl.src, pl.guid, (const float*)pl.z,
+                       (const float*)pl.maps, to, pl.err, *pl.w);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();

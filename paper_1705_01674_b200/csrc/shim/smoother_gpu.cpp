@@ -76,8 +76,23 @@ Image smooth(const Image& target, const Image& guidance, const SmoothConfig& cfg
 
 Image interpolate_sparse(const SparseField& field, const Image& guidance, const SmoothConfig& cfg,
                          Image* undefined_mask) {
+    // checks in the reference's order (proj/src/smoother.cpp:129-147): the field
+    // (first offending pixel in scan order), then smooth()'s config / empty /
+    // size checks -- so an input with several faults gets the reference's text
     if (field.mask.channels != 1) throw Error("interpolate_sparse: mask must be single-channel");
     if (!field.values.same_size(field.mask)) throw Error("interpolate_sparse: values/mask size mismatch");
+    bool any = false;
+    for (int y = 0; y < field.mask.height; ++y)
+        for (int x = 0; x < field.mask.width; ++x) {
+            const double mv = field.mask.at(y, x);
+            if (mv != 0.0 && mv != 1.0) throw Error("interpolate_sparse: mask must be 0/1");
+            if (mv == 1.0) any = true;
+            if (mv == 0.0)
+                for (int c = 0; c < field.values.channels; ++c)
+                    if (field.values.at(y, x, c) != 0.0) throw Error("interpolate_sparse: values nonzero outside mask");
+        }
+    if (!any) throw Error("interpolate_sparse: empty mask");
+    cfg.validate();
     if (field.values.empty()) throw Error("smooth: empty target");
     if (!field.values.same_size(guidance)) throw Error("smooth: target and guidance dimensions differ");
     const std::vector<float> v = to_f32(field.values), m = to_f32(field.mask), g = to_f32(guidance);

@@ -101,21 +101,51 @@ class DistExchange:
     def _global(self, peer: int) -> int:
         return self.dist.get_global_rank(self.group, peer) if self.group is not None else peer
 
+    def _staged(self, t) -> bool:
+        # gloo moves host memory: device tensors travel through host copies
+        return t.is_cuda and self.dist.get_backend(self.group) != "nccl"
+
     def run(self, sends, recvs) -> None:
         """sends/recvs: lists of (peer, tensor); one grouped exchange."""
         dist = self.dist
         if not sends and not recvs:
             return
-        ops = [dist.P2POp(dist.isend, t, self._global(p), self.group) for p, t in sends]
-        ops += [dist.P2POp(dist.irecv, t, self._global(p), self.group) for p, t in recvs]
         backend = dist.get_backend(self.group)
         if backend == "nccl":
+            ops = [dist.P2POp(dist.isend, t, self._global(p), self.group) for p, t in sends]
+            ops += [dist.P2POp(dist.irecv, t, self._global(p), self.group) for p, t in recvs]
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        else:  # gloo: plain isend/irecv pairs
-            works = [op.op(op.tensor, op.peer, op.group) for op in ops]
-            for w in works:
-                w.wait()
+            return
+        # gloo: plain isend/irecv pairs on host tensors
+        hs = [(p, t.contiguous().cpu() if self._staged(t) else t) for p, t in sends]
+        hr = [(p, t, t.new_empty(t.shape, device="cpu") if self._staged(t) else t) for p, t in recvs]
+        works = [dist.isend(h, self._global(p), self.group) for p, h in hs]
+        works += [dist.irecv(h, self._global(p), self.group) for p, _, h in hr]
+        for w in works:
+            w.wait()
+        for _, t, h in hr:
+            if h is not t:
+                t.copy_(h)
+
+    def broadcast(self, t, src: int) -> None:
+        """t (contiguous) from shard ``src`` to every shard, in place."""
+        if self._staged(t):
+            h = t.cpu()
+            self.dist.broadcast(h, src=self._global(src), group=self.group)
+            t.copy_(h)
+        else:
+            self.dist.broadcast(t, src=self._global(src), group=self.group)
+
+    def all_gather_int(self, v: int) -> list:
+        """Python ints (64-bit) of every shard."""
+        import torch
+
+        dev = "cuda" if self.dist.get_backend(self.group) == "nccl" else "cpu"
+        x = torch.tensor([v - (1 << 64) if v >= (1 << 63) else v], dtype=torch.int64, device=dev)
+        out = [torch.empty_like(x) for _ in range(self.nshards)]
+        self.dist.all_gather(out, x, group=self.group)
+        return [int(o.item()) & 0xFFFFFFFFFFFFFFFF for o in out]
 
 
 # ------------------------------------------------------------------ passes
@@ -256,13 +286,26 @@ class ShardedSmoother:
         w = self.win[lay][g]
         return self.tmp[g, lay][w.oa - w.s:w.ob - w.s]
 
+    def close(self) -> None:
+        """Release the CUDA graphs this smoother's passes captured (process-wide graph cache)."""
+        from .api import graph_clear
+
+        graph_clear()
+
     def run(self) -> None:
-        for p in range(self.T):
-            lay = self.layout(p)
-            for g in self.ex.local:
-                self.pass_fn(self.cur[g, lay], self.guid[g, lay], self.pcfg, self.tmp[g, lay])
-            if p + 1 < self.T:
-                self._transpose_exchange(lay)
+        import contextlib
+
+        import torch
+
+        # the native calls launch on the current device: make it this smoother's
+        ctx = torch.cuda.device(self.device) if self.device.type == "cuda" else contextlib.nullcontext()
+        with ctx:
+            for p in range(self.T):
+                lay = self.layout(p)
+                for g in self.ex.local:
+                    self.pass_fn(self.cur[g, lay], self.guid[g, lay], self.pcfg, self.tmp[g, lay])
+                if p + 1 < self.T:
+                    self._transpose_exchange(lay)
 
     def _transpose_exchange(self, lay: int) -> None:
         nxt = 1 - lay

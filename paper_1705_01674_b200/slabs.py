@@ -63,9 +63,10 @@ def _transpose(src, dst) -> None:
 
     h, w, c = src.shape
     err = N.errbuf()
-    st = torch.cuda.current_stream(src.device).cuda_stream
-    N.check(N.lib().sgwls_b200_transpose_device(src.data_ptr(), dst.data_ptr(), 1, w, h, c, C.c_void_p(st), err,
-                                                len(err)), err)
+    with torch.cuda.device(src.device):
+        st = torch.cuda.current_stream(src.device).cuda_stream
+        N.check(N.lib().sgwls_b200_transpose_device(src.data_ptr(), dst.data_ptr(), 1, w, h, c, C.c_void_p(st), err,
+                                                    len(err)), err)
 
 
 class SlabSmoother:
@@ -120,6 +121,8 @@ class SlabSmoother:
             self.work[g] = torch.empty(max(work, 1), **f32)
         self.recn = recn
         self.allrec = {g: torch.empty((self.G, recn), **f32) for g in self.ex.local}
+        # first-pass pivot-failure word per local slab (sgwls_b200_slab_pass_b)
+        self.errw = {g: torch.full((1,), -1, dtype=torch.int64, device=dev) for g in self.ex.local}
 
     @staticmethod
     def _hwc(a):
@@ -192,7 +195,7 @@ class SlabSmoother:
         s = self.win[g].s
         return self.buf[g][k][a - s:b - s]
 
-    def _column_pass(self) -> None:
+    def _column_pass(self, first: bool = False) -> None:
         nxt = self.cur ^ 1
         err = N.errbuf()
         for g in self.ex.local:
@@ -210,20 +213,23 @@ class SlabSmoother:
             guid = self._guid_rows(g)
             out = self._own(g, nxt)
             st = C.c_void_p(self._stream(g))
+            ew = self.errw[g].data_ptr() if first else None
             N.check(N.lib().sgwls_b200_slab_pass_b(src.data_ptr(), guid.data_ptr(), self.W, b - a, self.C, self.Cg,
                                                    a, self.G, g, C.byref(self.nc), self.work[g].data_ptr(),
-                                                   self.allrec[g].data_ptr(), out.data_ptr(), st, err, len(err)), err)
+                                                   self.allrec[g].data_ptr(), out.data_ptr(), ew, st, err,
+                                                   len(err)), err)
         self.cur = nxt
 
-    def _row_pass(self) -> None:
+    def _row_pass(self, first: bool = False) -> None:
         from .api import pass_device
 
         self._halo_exchange()
         nxt = self.cur ^ 1
         for g in self.ex.local:
             _transpose(self.buf[g][self.cur], self.tmpT[g])
-            # Column pass on the transposed window, written transposed: rows [s, e) of the image
-            pass_device(self.tmpT[g], self.gwinT[g], self.pcfg, out=self.buf[g][nxt], graph=True)
+            # Column pass on the transposed window, written transposed: rows [s, e) of the image.
+            # A first (row) pass synchronises to report the reference's pivot failure.
+            pass_device(self.tmpT[g], self.gwinT[g], self.pcfg, out=self.buf[g][nxt], graph=True, sync=first)
         self.cur = nxt
 
     def _stream(self, g: int) -> int:
@@ -268,12 +274,36 @@ class SlabSmoother:
                     recvs.append((h, self.buf[g][k][lo - self.win[g].s:hi - self.win[g].s]))
         self.ex.run(sends, recvs)
 
+    def close(self) -> None:
+        """Release the CUDA graphs this smoother's passes captured (process-wide graph cache)."""
+        from .api import graph_clear
+
+        graph_clear()
+
     def run(self) -> None:
-        for p in range(self.T):
-            if ((self.fa + p) & 1) == 0:
-                self._column_pass()
-            else:
-                self._row_pass()
+        import torch
+
+        # the native calls launch on the current device: make it this smoother's
+        with torch.cuda.device(self.device):
+            for g in self.ex.local:
+                self.errw[g].fill_(-1)
+            for p in range(self.T):
+                if ((self.fa + p) & 1) == 0:
+                    self._column_pass(first=p == 0)
+                else:
+                    self._row_pass(first=p == 0)
+
+    def check_errors(self) -> None:
+        """Raise the reference's pivot failure (proj/src/banded.cpp:66-68) if the
+        first pass met one on any slab: the smallest (line, position) key wins,
+        as in the unsharded filter.  Synchronises (and, distributed, gathers the
+        keys of all ranks)."""
+        keys = [int(self.errw[g].item()) & 0xFFFFFFFFFFFFFFFF for g in self.ex.local]
+        if len(self.ex.local) < self.G:
+            keys = self.ex.all_gather_int(min(keys))
+        key = min(keys)
+        if key != 0xFFFFFFFFFFFFFFFF:
+            raise Error(f"rband_lu_factorize: non-positive pivot at row {key & 0xFFFFFFFF} (input not SPD)")
 
     def owned(self, g: int | None = None):
         """(first, last, rows): slab g's rows [first, last) of the result (H-major layout)."""
@@ -282,20 +312,19 @@ class SlabSmoother:
         return a, b, self._own(g, self.cur)
 
     def gather(self):
-        """Full (H, W, C) result on every process."""
+        """Full (H, W, C) result on every process (raises the first pass's pivot failure)."""
         import torch
 
+        self.check_errors()
         full = torch.empty((self.H, self.W, self.C), dtype=torch.float32, device=self.device)
         for g in self.ex.local:
             a, b, t = self.owned(g)
             full[a:b].copy_(t)
         if len(self.ex.local) < self.G:
-            import torch.distributed as dist
-
             for g in range(self.G):
                 a, b = self.slabs[g]
                 part = full[a:b].contiguous()
-                dist.broadcast(part, src=self.ex._global(g), group=self.ex.group)
+                self.ex.broadcast(part, g)
                 full[a:b].copy_(part)
         return full
 

@@ -68,6 +68,27 @@ int main(int argc, char** argv) {
         } catch (const Error& e) {
             std::printf("error: %s\n", e.what());
         }
+        // several faults at once: the reference reports the field check first
+        // (bad mask value) before smooth()'s guidance-size check
+        try {
+            SparseField f{Image(8, 6, 1, 0.0), Image(8, 6, 1, 0.0)};
+            f.mask.at(2, 3) = 0.5;
+            f.values.at(4, 4) = 1.0;
+            interpolate_sparse(f, Image(9, 6, 1, 0.5), SmoothConfig{});
+        } catch (const Error& e) {
+            std::printf("error: %s\n", e.what());
+        }
+        // values off the mask before an invalid configuration
+        try {
+            SparseField f{Image(8, 6, 1, 0.0), Image(8, 6, 1, 0.0)};
+            f.mask.at(0, 0) = 1.0;
+            f.values.at(1, 1) = 2.0;
+            SmoothConfig bad;
+            bad.r = 0;
+            interpolate_sparse(f, Image(8, 6, 1, 0.5), bad);
+        } catch (const Error& e) {
+            std::printf("error: %s\n", e.what());
+        }
     } catch (const std::exception& e) {
         std::fprintf(stderr, "failed: %s\n", e.what());
         return 1;

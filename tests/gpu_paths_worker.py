@@ -1,6 +1,6 @@
 """Subprocess body of tests/test_gpu_paths.py: parity of the tiled pass under
-one forced kernel schedule (SGWLS_KC / SGWLS_KA_WARPS / SGWLS_TILE_WARPS /
-SGWLS_FUSE_K2 are read once per process).  Prints the max |delta| per case."""
+one forced kernel schedule (SGWLS_KA_WARPS / SGWLS_TILE_WARPS / SGWLS_K2_NG /
+SGWLS_PDL are read once per process).  Prints the max |delta| per case."""
 import os
 import sys
 

@@ -188,8 +188,8 @@ def test_graph_replay_matches_direct():
 
 # ------------------------------------------------ BASELINE configurations
 
-def _full(name, port, max_images=None):
-    wl = WL.workload(name)
+def _full(name, port, max_images=None, secondary=False):
+    wl = WL.workload(name, secondary=secondary)
     cfg = wl.cfg.copy(threads=NTHREADS)
     gen = WL.GENERATORS[name]
     if wl.sparse:
@@ -220,3 +220,36 @@ def test_baseline_c5_parity(port):
     err = _full("c5", port)
     print(f"c5: max|d| = {err:.3g}")
     assert err <= TOL
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_baseline_secondary_reading_parity(name, port):
+    """SURVEY.md 8(d) secondary reading: iterations = tau sweeps at stride 1."""
+    err = _full(name, port, max_images=1, secondary=True)
+    print(f"{name} (iterations = tau, tau = 1): max|d| = {err:.3g}")
+    assert err <= TOL
+
+
+@pytest.mark.slow
+def test_c4_batch_parity_16_pairs(port):
+    """c4 through the batched device path the bench times: 16 of the 64 pairs
+    (every 4th) in ONE interpolate_sparse_device call, each pair against the
+    oracle, with the reference's field validation on the device."""
+    import torch
+
+    wl = WL.workload("c4")
+    cfg = wl.cfg.copy(threads=NTHREADS)
+    ids = list(range(0, 64, 4))
+    trip = [WL.gen_c4(i) for i in ids]
+    dv, dm, dg = (torch.from_numpy(np.stack([t[k] for t in trip])).cuda() for k in range(3))
+    und = torch.empty_like(dm)
+    out = S.interpolate_sparse_device(dv, dm, dg, cfg, undefined=und, validate=True, sync=True)
+    out, und = out.cpu().numpy(), und.cpu().numpy()
+    worst = 0.0
+    for k, (v, m, g) in enumerate(trip):
+        want, wund = port.interpolate_sparse(v, m, g, cfg)
+        worst = max(worst, float(np.abs(out[k] - want.reshape(out[k].shape)).max()))
+        assert (und[k] == wund).all(), ids[k]
+    print(f"c4 pairs {ids}: max|d| = {worst:.3g}")
+    assert worst <= TOL

@@ -1,6 +1,6 @@
-"""Every kernel schedule of the tiled pass against the oracle: KB solving its
-tile's inner separators vs the separate KC launch, KA/KB tile heights, K2 fused
-into KA, KB waiting on per-band-group ready flags, both grid orders.  The schedule is chosen per radius by default, so each forced choice
+"""Every kernel schedule of the tiled pass against the oracle: KA tile heights
+(the tiles KA's separator maps span) independent of the KB tile heights, K2
+tree widths, programmatic dependent launch on and off.  The schedule is chosen per radius by default, so each forced choice
 runs in its own process (the knobs are read once)."""
 import os
 import subprocess
@@ -11,14 +11,13 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 SCHEDULES = [
-    {"SGWLS_KC": "0"},
-    {"SGWLS_KC": "1"},
-    {"SGWLS_KC": "1", "SGWLS_KA_WARPS": "4", "SGWLS_TILE_WARPS": "8"},
-    {"SGWLS_KC": "0", "SGWLS_TILE_WARPS": "2"},
-    {"SGWLS_KC": "0", "SGWLS_FUSE_K2": "1"},
-    {"SGWLS_KC": "0", "SGWLS_FLAGS": "1"},
-    {"SGWLS_KC": "0", "SGWLS_FLAGS": "1", "SGWLS_KA_JFAST": "1", "SGWLS_KB_JFAST": "1"},
-    {"SGWLS_KC": "1", "SGWLS_FUSE_K2": "1", "SGWLS_KA_WARPS": "2"},
+    {"SGWLS_PDL": "1"},
+    {"SGWLS_PDL": "0"},
+    {"SGWLS_KA_WARPS": "4", "SGWLS_TILE_WARPS": "8"},
+    {"SGWLS_KA_WARPS": "8", "SGWLS_TILE_WARPS": "2"},
+    {"SGWLS_KA_WARPS": "3", "SGWLS_TILE_WARPS": "5", "SGWLS_K2_NG": "4"},
+    {"SGWLS_KA_WARPS": "2", "SGWLS_K2_NG": "16"},
+    {"SGWLS_KA_WARPS": "1"},
 ]
 
 

@@ -129,3 +129,84 @@ def test_gpu_slabs_match_unsharded(G, cfg, shape, port):
     print(f"slabs G={G} {shape} r={cfg.r}: max|d| vs unsharded GPU {d_dev:.2e}, vs oracle {d_ref:.2e}")
     assert d_ref < 1e-4
     assert d_dev < 2e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fa", [Axis.Column, Axis.Row])
+def test_gpu_slabs_report_pivot_failure(fa, port):
+    """A NaN guidance sample is the reference's "non-positive pivot at row k"
+    (proj/src/banded.cpp:66-68): the slab filter reports the same text."""
+    import paper_1705_01674_b200 as S
+    from oracle.pyoracle import OracleError
+
+    h, w = 120, 90
+    t = _img(h, w, 1, seed=4)
+    g = _img(h, w, 1, seed=5)
+    g[77, 41, 0] = np.nan  # in the third of three slabs
+    cfg = _cfg(r=2, tau=3, T=2, fa=fa)
+    with pytest.raises(OracleError) as want:
+        port.smooth(t, g, cfg)
+    sm = SlabSmoother(h, w, 1, 1, cfg, exchange=LocalExchange(3), device="cuda")
+    sm.load(t, g)
+    with pytest.raises(S.Error) as got:
+        sm.run()
+        sm.gather()
+    assert str(got.value) == str(want.value)
+
+
+def _gloo_gpu_worker(rank, world, port_no, q):
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port_no)
+    torch.cuda.set_device(0)  # both ranks share the one GPU; gloo stages through host memory
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1705_01674_b200.slabs import DistExchange
+
+        h, w = 301, 130
+        cfg = _cfg(r=2, tau=3, T=4)
+        t = _img(h, w, 1, seed=21)
+        g = _img(h, w, 1, seed=22)
+        sm = SlabSmoother(h, w, 1, 1, cfg, exchange=DistExchange(), device="cuda:0")
+        sm.load(t, g)
+        sm.run()
+        out = sm.gather().cpu().numpy()
+        sm.close()
+        if rank == 0:
+            np.save(os.environ["SGWLS_TEST_OUT"], out)
+        q.put((rank, "ok"))
+    except Exception as e:  # reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_gpu_slabs_two_processes_dist_exchange(port, tmp_path):
+    """Two ranks (torch.distributed, gloo, both on cuda:0 -- the multi-rank code
+    path with real process boundaries) run a full T = 4 slab filter; the
+    gathered image matches the oracle."""
+    import torch.multiprocessing as mp
+
+    outp = str(tmp_path / "slab2.npy")
+    os.environ["SGWLS_TEST_OUT"] = outp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port_no = _free_port()
+    procs = [ctx.Process(target=_gloo_gpu_worker, args=(r, 2, port_no, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=120)
+    assert res == [(0, "ok"), (1, "ok")], res
+    h, w = 301, 130
+    t = _img(h, w, 1, seed=21)
+    g = _img(h, w, 1, seed=22)
+    want = port.smooth(t, g, _cfg(r=2, tau=3, T=4))
+    got = np.load(outp)
+    err = float(np.abs(got - want).max())
+    print(f"2-process slab filter vs oracle: {err:.2e}")
+    assert err <= 1e-4
