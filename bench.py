@@ -241,7 +241,9 @@ def main():
         if sharded:
             sm.run()
         elif wl.sparse:
-            S.interpolate_sparse_device(dv, dm, dg, cfg, out=dout, stream=stream, graph=use_graph)
+            # validate=True: the reference's field checks (proj/src/smoother.cpp:129-144) on every
+            # call, all pairs in one kernel + one host synchronisation, inside the timed region
+            S.interpolate_sparse_device(dv, dm, dg, cfg, out=dout, stream=stream, graph=use_graph, validate=True)
         else:
             S.smooth_device(dt, dg, cfg, out=dout, stream=stream, graph=use_graph)
 

@@ -172,6 +172,24 @@ int sgwls_b200_slab_pass_b(const float* d_src, const float* d_guidance, int widt
                            float* d_work, const float* d_records, float* d_out, unsigned long long* d_pivot_err,
                            void* stream, char* err, size_t errlen);
 
+/* ---- multi-GPU (one process driving several devices) ----
+ * sgwls::smooth of ONE image over `ndev` devices (devices[i] = CUDA ordinal of row
+ * slab i; repeats allowed): the row-slab partitioned solve of the slab API above,
+ * with the slab records all-gathered and the row-pass halos exchanged peer to peer
+ * (cudaMemcpyPeerAsync over NVLink).  Same result as sgwls_b200_smooth (exact).
+ * ndev <= 0: the devices listed in SGWLS_B200_DEVICES ("0,1,2,3"), else device 0.
+ * Geometry outside the slab mode (r > 4, clipped bands, 2/4 guidance channels, fewer
+ * rows than slabs) runs on the first device.  Host buffers, synchronous. */
+int sgwls_b200_smooth_multi(const float* target, int width, int height, int channels, const float* guidance,
+                            int guidance_channels, const sgwls_b200_config* cfg, const int* devices, int ndev,
+                            float* out, char* err, size_t errlen);
+/* `batch` independent interpolate_sparse pairs split over the devices (contiguous
+ * shares, one host thread per device); errors as the serial batch call. */
+int sgwls_b200_interpolate_sparse_batch_multi(const float* values, const float* masks, const float* guidances,
+                                              int batch, int width, int height, int channels, int guidance_channels,
+                                              const sgwls_b200_config* cfg, const int* devices, int ndev,
+                                              float* out, float* undefined_mask, char* err, size_t errlen);
+
 /* ---- application pipelines (proj/include/sgwls/apps.hpp, proj/src/apps.cpp) ----
  * The reference's four callers of the filter, with every stage on the device:
  * one upload, the smooth() / interpolate_sparse() passes and the elementwise

@@ -104,6 +104,12 @@ SIGNATURES = {
                                          C.POINTER(NativeConfig), _P, _P, _P, C.c_char_p, C.c_size_t]),
     "sgwls_b200_slab_pass_b": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(NativeConfig), _P, _P, _P, _P, _P, C.c_char_p, C.c_size_t]),
+    # multi-GPU, one process
+    "sgwls_b200_smooth_multi": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, _P, C.c_int, C.POINTER(NativeConfig), _P,
+                                          C.c_int, _P, C.c_char_p, C.c_size_t]),
+    "sgwls_b200_interpolate_sparse_batch_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                            C.POINTER(NativeConfig), _P, C.c_int, _P, _P, C.c_char_p,
+                                                            C.c_size_t]),
     # application pipelines (proj/src/apps.cpp)
     "sgwls_b200_enhance_preset": (None, [C.POINTER(NativeConfig)]),
     "sgwls_b200_tonemap_layer_preset": (None, [C.c_double, C.POINTER(NativeConfig)]),

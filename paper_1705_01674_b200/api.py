@@ -73,6 +73,28 @@ def smooth_batch(targets, guidances, cfg: SmoothConfig | None = None) -> np.ndar
     return out[..., 0] if squeeze else out
 
 
+def smooth_multi(target, guidance, cfg: SmoothConfig | None = None, devices=None) -> np.ndarray:
+    """``smooth`` of ONE image in row slabs over several GPUs of this process
+    (``sgwls_b200_smooth_multi``: slab records all-gathered, halos exchanged peer
+    to peer).  devices: CUDA ordinals, one per slab (repeats allowed); None = the
+    SGWLS_B200_DEVICES list, else device 0."""
+    cfg = cfg or SmoothConfig()
+    squeeze = np.asarray(target).ndim == 2
+    t = _as_hwc(target, "smooth")
+    g = _as_hwc(guidance, "smooth")
+    _check_same_size(t, g)
+    h, w, c = t.shape
+    out = np.empty_like(t)
+    err = N.errbuf()
+    nc = N.to_native(cfg)
+    devs = np.ascontiguousarray(devices if devices is not None else [], dtype=np.int32)
+    rc = N.lib().sgwls_b200_smooth_multi(t.ctypes.data, w, h, c, g.ctypes.data, g.shape[2], C.byref(nc),
+                                         devs.ctypes.data if devs.size else None, int(devs.size), out.ctypes.data,
+                                         err, len(err))
+    N.check(rc, err)
+    return out[:, :, 0] if squeeze else out
+
+
 def interpolate_sparse(field: SparseField, guidance, cfg: SmoothConfig | None = None,
                        return_undefined: bool = False):
     """Guided interpolation smooth(values)/smooth(mask) (Eq. 21)."""

@@ -20,6 +20,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/sgwls_b200.h"
@@ -319,9 +320,21 @@ void require_device() {
 // pass_only: exactly one Column-axis pass (proj/src/smoother.cpp:51-99) whose
 // output is written in the transposed layout (the building block of the
 // line-slab sharded filter, sharded.py).
+// Sparse hooks (interpolate_sparse, proj/src/smoother.cpp:146-161): d_mask !=
+// nullptr -> d_t holds C-1 value channels and the mask is channel C-1 (read
+// split by the first pass); ratio -> d_out gets C-1 channels num/den and d_und
+// the undefined mask, computed in the last pass's epilogue.  Both only where
+// run_smooth_sparse_fusable() says the tiled path runs those passes.
+struct SparseHooks {
+    const float* d_mask = nullptr;
+    bool ratio = false;
+    float floor_ = 0.f;
+    float* d_und = nullptr;
+};
+
 void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int C, int Cg,
                 const sgwls_b200_config* cfg, float* d_out, unsigned long long* d_err, cudaStream_t st,
-                bool pass_only = false) {
+                bool pass_only = false, const SparseHooks* sh = nullptr) {
     WeightDev wd;
     build_weights(cfg, wd);
     const int T = pass_only ? 1 : cfg->iterations;
@@ -400,9 +413,26 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.U = U.p;
         pl.err = (p == 0) ? d_err : nullptr;
         pl.w = &wd;
+        if (sh && p == 0 && sh->d_mask) pl.geom.msk = sh->d_mask;
+        if (sh && lastp && sh->ratio) {
+            pl.ratio = 1;
+            pl.ratio_floor = sh->floor_;
+            pl.und = sh->d_und;
+        }
         CK(launch_pass(pl, st));
         src = out;
     }
+}
+
+// Can interpolate_sparse read values + mask unpacked in its first pass and
+// fuse the ratio into its last (both passes on the tiled path, first pass on
+// the caller's layout)?
+void sparse_fusable(int batch, int W, int H, int C, int Cg, const sgwls_b200_config* cfg, bool& split, bool& ratio) {
+    const int T = cfg->iterations, fa = cfg->first_axis;
+    const AxisPlan ap0 = plan_axis(H, W, C, Cg, cfg->r, cfg->tau, batch);
+    const AxisPlan ap1 = plan_axis(W, H, C, Cg, cfg->r, cfg->tau, batch);
+    split = fa == 0 && ap0.fast;
+    ratio = (((fa + T - 1) & 1) == 0 ? ap0 : ap1).fast;
 }
 
 std::string pivot_message(unsigned long long key) {
@@ -423,26 +453,28 @@ struct ErrWord {
     }
 };
 
-// Sparse validation in the reference's order (proj/src/smoother.cpp:129-144).
+// Sparse validation in the reference's order (proj/src/smoother.cpp:129-144),
+// every pair in one launch and one host synchronisation; the first failing
+// pair (in batch order) decides the error, as the reference's per-call checks.
 void validate_sparse(const float* d_v, const float* d_m, int batch, long long npx, int C, cudaStream_t st) {
     unsigned long long* status = nullptr;
-    CK(cudaMallocAsync((void**)&status, 2 * sizeof(unsigned long long), st));
-    unsigned long long h[2];
+    CK(cudaMallocAsync((void**)&status, 2 * (size_t)batch * sizeof(unsigned long long), st));
+    std::vector<unsigned long long> h(2 * (size_t)batch);
     try {
+        CK(cudaMemsetAsync(status, 0xff, (size_t)batch * sizeof(unsigned long long), st));
+        CK(cudaMemsetAsync(status + batch, 0, (size_t)batch * sizeof(unsigned long long), st));
+        CK(launch_validate_sparse(d_v, d_m, npx, C, batch, status, st));
+        CK(cudaMemcpyAsync(h.data(), status, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         for (int b = 0; b < batch; ++b) {
-            CK(cudaMemsetAsync(status, 0xff, sizeof(unsigned long long), st));
-            CK(cudaMemsetAsync(status + 1, 0, sizeof(unsigned long long), st));
-            CK(launch_validate_sparse(d_v + (size_t)b * npx * C, d_m + (size_t)b * npx, npx, C, status, st));
-            CK(cudaMemcpyAsync(h, status, sizeof h, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (h[0] != ULLONG_MAX) {
+            if (h[b] != ULLONG_MAX) {
                 // which violation? read that pixel's mask
                 float mv = 0.f;
-                CK(cudaMemcpy(&mv, d_m + (size_t)b * npx + h[0], sizeof(float), cudaMemcpyDeviceToHost));
+                CK(cudaMemcpy(&mv, d_m + (size_t)b * npx + h[b], sizeof(float), cudaMemcpyDeviceToHost));
                 if (mv != 0.f && mv != 1.f) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: mask must be 0/1"};
                 throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: values nonzero outside mask"};
             }
-            if (h[1] == 0) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
+            if (h[batch + b] == 0) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
         }
     } catch (...) {
         cudaFreeAsync(status, st);
@@ -455,14 +487,30 @@ void run_sparse(const float* d_v, const float* d_m, const float* d_g, int batch,
                 const sgwls_b200_config* cfg, float* d_out, float* d_und, unsigned long long* d_err,
                 cudaStream_t st) {
     const long long npx = (long long)batch * W * H;
-    DevBuf packed, res;
-    packed.alloc((size_t)npx * (C + 1), st);
-    res.alloc((size_t)npx * (C + 1), st);
-    CK(launch_pack_sparse(d_v, d_m, packed.p, npx, C, st));
     // num = smooth(values), den = smooth(mask) share every factorization: one
-    // (C+1)-channel smooth (proj/src/smoother.cpp:146-147).
-    run_smooth(packed.p, d_g, batch, W, H, C + 1, Cg, cfg, res.p, d_err, st);
-    CK(launch_ratio(res.p, d_out, d_und, npx, C, (float)kMaskFloor, st));
+    // (C+1)-channel smooth (proj/src/smoother.cpp:146-147); on the tiled path the
+    // first pass reads values and mask where they lie and the last pass writes
+    // the ratio (proj/src/smoother.cpp:149-161) -- no pack / ratio kernels
+    bool split = false, ratio = false;
+    sparse_fusable(batch, W, H, C + 1, Cg, cfg, split, ratio);
+    DevBuf packed, res;
+    SparseHooks sh;
+    if (split) {
+        sh.d_mask = d_m;
+    } else {
+        packed.alloc((size_t)npx * (C + 1), st);
+        CK(launch_pack_sparse(d_v, d_m, packed.p, npx, C, st));
+    }
+    if (ratio) {
+        sh.ratio = true;
+        sh.floor_ = (float)kMaskFloor;
+        sh.d_und = d_und;
+    } else {
+        res.alloc((size_t)npx * (C + 1), st);
+    }
+    run_smooth(split ? d_v : packed.p, d_g, batch, W, H, C + 1, Cg, cfg, ratio ? d_out : res.p, d_err, st, false,
+               &sh);
+    if (!ratio) CK(launch_ratio(res.p, d_out, d_und, npx, C, (float)kMaskFloor, st));
 }
 
 void finish_sync(unsigned long long* d_err, cudaStream_t st) {
@@ -472,6 +520,23 @@ void finish_sync(unsigned long long* d_err, cudaStream_t st) {
     if (h != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(h)};
 }
 
+
+// host buffers -> device -> T passes -> host, on the calling thread's stream
+void smooth_host(const float* t, const float* g, int batch, int width, int height, int channels, int gch,
+                 const sgwls_b200_config* cfg, float* out) {
+    cudaStream_t st = cudaStreamPerThread;
+    const size_t nt = (size_t)batch * width * height * channels, ng = (size_t)batch * width * height * gch;
+    DevBuf dt, dg, dout;
+    dt.alloc(nt, st);
+    dg.alloc(ng, st);
+    dout.alloc(nt, st);
+    CK(cudaMemcpyAsync(dt.p, t, nt * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dg.p, g, ng * 4, cudaMemcpyHostToDevice, st));
+    ErrWord ew(st);
+    run_smooth(dt.p, dg.p, batch, width, height, channels, gch, cfg, dout.p, ew.d, st);
+    CK(cudaMemcpyAsync(out, dout.p, nt * 4, cudaMemcpyDeviceToHost, st));
+    finish_sync(ew.d, st);
+}
 
 // ------------------------------------------------------ CUDA-graph replay
 //
@@ -765,18 +830,7 @@ int sgwls_b200_smooth_batch(const float* t, const float* g, int batch, int width
         rc = check_shape(batch, width, height, channels, gch, msg);
         if (rc) throw Fail{rc, msg};
         require_device();
-        cudaStream_t st = cudaStreamPerThread;
-        const size_t nt = (size_t)batch * width * height * channels, ng = (size_t)batch * width * height * gch;
-        DevBuf dt, dg, dout;
-        dt.alloc(nt, st);
-        dg.alloc(ng, st);
-        dout.alloc(nt, st);
-        CK(cudaMemcpyAsync(dt.p, t, nt * 4, cudaMemcpyHostToDevice, st));
-        CK(cudaMemcpyAsync(dg.p, g, ng * 4, cudaMemcpyHostToDevice, st));
-        ErrWord ew(st);
-        run_smooth(dt.p, dg.p, batch, width, height, channels, gch, cfg, dout.p, ew.d, st);
-        CK(cudaMemcpyAsync(out, dout.p, nt * 4, cudaMemcpyDeviceToHost, st));
-        finish_sync(ew.d, st);
+        smooth_host(t, g, batch, width, height, channels, gch, cfg, out);
     });
 }
 
@@ -867,7 +921,11 @@ int sgwls_b200_kernel_launches(int width, int height, int channels, int gch, int
     if (fa == 1 || T >= 2) n += 1;  // guidance transpose
     if (fa == 1) n += 1;            // input transpose
     for (int p = 0; p < T; ++p) n += kernels_per_pass(((fa + p) & 1) == 0 ? ap0 : ap1);
-    if (sparse) n += 2;  // pack + ratio
+    if (sparse) {  // pack / ratio kernels unless the tiled passes read the field unpacked and fuse the ratio
+        bool split = false, ratio = false;
+        sparse_fusable(batch, width, height, C, gch, cfg, split, ratio);
+        n += (split ? 0 : 1) + (ratio ? 0 : 1);
+    }
     return n;
 }
 
@@ -1174,6 +1232,325 @@ int sgwls_b200_colorize(const float* gray, int gray_channels, const float* scrib
         CK(launch_colorize_out(dgray.p, dres.p, dout.p, npx, st));
         CK(cudaMemcpyAsync(out, dout.p, npx * 3 * 4, cudaMemcpyDeviceToHost, st));
         finish_sync(ew.d, st);
+    });
+}
+
+}  // extern "C"
+
+// ====================================================== multi-GPU (row slabs)
+//
+// sgwls::smooth of ONE image over several GPUs driven from this process: the
+// row-slab mode of sgwls_tile.cuh (paper_1705_01674_b200/slabs.py is the same
+// schedule over torch.distributed ranks).  Device i keeps image rows
+// [a_i, a_{i+1}) for the whole filter.  A Column pass is the exact partitioned
+// solve: phase A (KA + one slab record per band) on every device, an
+// all-gather of the slab records (cudaMemcpyPeerAsync: NVLink P2P when the
+// devices can reach each other, staged by the driver otherwise), phase B
+// (slab separators, KB) -- only ~G*bands*REC floats cross GPUs.  A Row pass
+// runs each device's row window [s_i, e_i) (its slab plus a halo of <= 2r+1
+// rows, exchanged peer to peer) as an ordinary pass on the transposed window.
+// Every device works on its own stream; pass boundaries are cross-device event
+// barriers.  The same device may appear several times (slabs on one GPU).
+namespace {
+
+struct SlabDev {
+    int dev = 0, a = 0, b = 0, s = 0, e = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev = nullptr;
+    float* buf[2] = {nullptr, nullptr};  // row window [s, e) x W x C, ping-pong
+    float* gwin = nullptr;               // guidance rows [s, e)
+    float* gwinT = nullptr;              // transposed guidance window (W x (e-s))
+    float* tmpT = nullptr;               // transposed image window
+    float* work = nullptr;               // slab-pass workspace
+    float* allrec = nullptr;             // G slab records
+    unsigned long long* err = nullptr;   // first-pass pivot report
+};
+
+struct DevGuard {
+    int saved = 0;
+    DevGuard() { cudaGetDevice(&saved); }
+    ~DevGuard() { cudaSetDevice(saved); }
+};
+
+class MultiSlab {
+   public:
+    MultiSlab(const int* devices, int ndev, int W, int H, int C, int Cg, const sgwls_b200_config* cfg)
+        : W_(W), H_(H), C_(C), Cg_(Cg), cfg_(*cfg), G_(ndev) {
+        pcfg_ = cfg_;
+        pcfg_.iterations = 1;
+        pcfg_.first_axis = SGWLS_B200_AXIS_COLUMN;
+        build_weights(&pcfg_, wd_);
+        const int r = cfg->r, tau = cfg->tau;
+        sl_.resize(G_);
+        for (int g = 0; g < G_; ++g) {  // slabs with even starts (serpentine parity), as slabs.slab_rows
+            sl_[g].dev = devices[g];
+            sl_[g].a = 2 * (int)(((long long)g * H) / (2LL * G_));
+        }
+        for (int g = 0; g < G_; ++g) {
+            SlabDev& d = sl_[g];
+            d.b = g + 1 < G_ ? sl_[g + 1].a : H;
+            if (d.b <= d.a) throw Fail{SGWLS_B200_EINVAL, "sgwls_b200: image too short for " + std::to_string(G_) + " row slabs"};
+            d.s = d.a == 0 ? 0 : ((d.a - 2 * r > 0 ? d.a - 2 * r : 0) / tau) * tau;
+            d.e = d.b == H ? H : (d.b + 2 * r + 1 < H ? d.b + 2 * r + 1 : H);
+        }
+    }
+    // allocation separate from construction: a failure part-way is cleaned up by the destructor
+    void init() {
+        const int W = W_, C = C_, Cg = Cg_;
+        for (int g = 0; g < G_; ++g) {
+            SlabDev& d = sl_[g];
+            CK(cudaSetDevice(d.dev));
+            init_pool_once_dev(d.dev);
+            CK(cudaStreamCreateWithFlags(&d.st, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&d.ev, cudaEventDisableTiming));
+            const size_t ws = (size_t)(d.e - d.s) * W;
+            CK(cudaMalloc((void**)&d.buf[0], ws * C * 4));
+            CK(cudaMalloc((void**)&d.buf[1], ws * C * 4));
+            CK(cudaMalloc((void**)&d.gwin, ws * Cg * 4));
+            CK(cudaMalloc((void**)&d.gwinT, ws * Cg * 4));
+            CK(cudaMalloc((void**)&d.tmpT, ws * C * 4));
+            const SlabLayout L = slab_layout(W, d.b - d.a, C, Cg, &pcfg_, G_);
+            recn_ = L.record;
+            CK(cudaMalloc((void**)&d.work, (L.total ? L.total : 1) * 4));
+            CK(cudaMalloc((void**)&d.allrec, (size_t)G_ * L.record * 4));
+            CK(cudaMalloc((void**)&d.err, sizeof(unsigned long long)));
+            for (int h = 0; h < G_; ++h)  // P2P where the topology allows it (errors: already on / unsupported)
+                if (sl_[h].dev != d.dev && cudaDeviceEnablePeerAccess(sl_[h].dev, 0) != cudaSuccess)
+                    cudaGetLastError();
+        }
+    }
+    ~MultiSlab() {
+        for (SlabDev& d : sl_) {
+            cudaSetDevice(d.dev);
+            if (d.st) cudaStreamSynchronize(d.st);
+            for (float* p : {d.buf[0], d.buf[1], d.gwin, d.gwinT, d.tmpT, d.work, d.allrec}) cudaFree(p);
+            cudaFree(d.err);
+            if (d.ev) cudaEventDestroy(d.ev);
+            if (d.st) cudaStreamDestroy(d.st);
+        }
+    }
+
+    void run(const float* target, const float* guidance, float* out) {
+        const size_t rowC = (size_t)W_ * C_, rowG = (size_t)W_ * Cg_;
+        for (SlabDev& d : sl_) {  // upload: own rows + guidance window
+            CK(cudaSetDevice(d.dev));
+            CK(cudaMemsetAsync(d.err, 0xff, sizeof(unsigned long long), d.st));
+            CK(cudaMemcpyAsync(d.buf[0] + (size_t)(d.a - d.s) * rowC, target + (size_t)d.a * rowC,
+                               (size_t)(d.b - d.a) * rowC * 4, cudaMemcpyHostToDevice, d.st));
+            CK(cudaMemcpyAsync(d.gwin, guidance + (size_t)d.s * rowG, (size_t)(d.e - d.s) * rowG * 4,
+                               cudaMemcpyHostToDevice, d.st));
+            CK(launch_transpose(d.gwin, d.gwinT, d.e - d.s, W_, Cg_, 1, d.st));
+        }
+        int cur = 0;
+        for (int p = 0; p < cfg_.iterations; ++p) {
+            const bool column = ((cfg_.first_axis + p) & 1) == 0;
+            if (column)
+                column_pass(cur, p == 0);
+            else
+                row_pass(cur, p == 0);
+            cur ^= 1;
+        }
+        for (SlabDev& d : sl_) {  // download own rows
+            CK(cudaSetDevice(d.dev));
+            CK(cudaMemcpyAsync(out + (size_t)d.a * rowC, d.buf[cur] + (size_t)(d.a - d.s) * rowC,
+                               (size_t)(d.b - d.a) * rowC * 4, cudaMemcpyDeviceToHost, d.st));
+        }
+        unsigned long long key = ULLONG_MAX;
+        for (SlabDev& d : sl_) {
+            CK(cudaSetDevice(d.dev));
+            unsigned long long h = ULLONG_MAX;
+            CK(cudaMemcpyAsync(&h, d.err, sizeof h, cudaMemcpyDeviceToHost, d.st));
+            CK(cudaStreamSynchronize(d.st));
+            if (h < key) key = h;
+        }
+        if (key != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(key)};
+    }
+
+   private:
+    // every stream waits for every other stream's work so far
+    void barrier() {
+        for (SlabDev& d : sl_) {
+            CK(cudaSetDevice(d.dev));
+            CK(cudaEventRecord(d.ev, d.st));
+        }
+        for (SlabDev& d : sl_) {
+            CK(cudaSetDevice(d.dev));
+            for (SlabDev& o : sl_)
+                if (&o != &d) CK(cudaStreamWaitEvent(d.st, o.ev, 0));
+        }
+    }
+
+    void column_pass(int cur, bool first) {
+        const size_t rowC = (size_t)W_ * C_, rowG = (size_t)W_ * Cg_;
+        for (int g = 0; g < G_; ++g) {  // phase A: chunk records + this slab's record
+            SlabDev& d = sl_[g];
+            CK(cudaSetDevice(d.dev));
+            const SlabLayout L = slab_layout(W_, d.b - d.a, C_, Cg_, &pcfg_, G_);
+            PassLaunch pl = slab_launch(L, d.buf[cur] + (size_t)(d.a - d.s) * rowC, d.gwin + (size_t)(d.a - d.s) * rowG,
+                                        d.a, G_, g, d.work, &wd_, C_);
+            pl.slab_phase = 1;
+            pl.slabrec = d.allrec + (size_t)g * recn_;
+            CK(launch_pass(pl, d.st));
+        }
+        barrier();
+        for (int h = 0; h < G_; ++h) {  // all-gather of the slab records, pulled by each device
+            SlabDev& d = sl_[h];
+            CK(cudaSetDevice(d.dev));
+            for (int g = 0; g < G_; ++g)
+                if (g != h)
+                    CK(cudaMemcpyPeerAsync(d.allrec + (size_t)g * recn_, d.dev, sl_[g].allrec + (size_t)g * recn_,
+                                           sl_[g].dev, recn_ * 4, d.st));
+        }
+        barrier();
+        for (int g = 0; g < G_; ++g) {  // phase B: slab separators, chunk interiors, own rows
+            SlabDev& d = sl_[g];
+            CK(cudaSetDevice(d.dev));
+            const SlabLayout L = slab_layout(W_, d.b - d.a, C_, Cg_, &pcfg_, G_);
+            PassLaunch pl = slab_launch(L, d.buf[cur] + (size_t)(d.a - d.s) * rowC, d.gwin + (size_t)(d.a - d.s) * rowG,
+                                        d.a, G_, g, d.work, &wd_, C_);
+            pl.slab_phase = 2;
+            pl.slabrec = d.allrec;
+            pl.out = d.buf[cur ^ 1] + (size_t)(d.a - d.s) * rowC;
+            pl.err = first ? d.err : nullptr;
+            CK(launch_pass(pl, d.st));
+        }
+    }
+
+    void row_pass(int cur, bool first) {
+        const size_t rowC = (size_t)W_ * C_;
+        barrier();
+        for (int h = 0; h < G_; ++h) {  // halo rows: window rows of h owned by other slabs
+            SlabDev& d = sl_[h];
+            CK(cudaSetDevice(d.dev));
+            for (int g = 0; g < G_; ++g) {
+                if (g == h) continue;
+                const SlabDev& o = sl_[g];
+                const int lo = o.a > d.s ? o.a : d.s, hi = o.b < d.e ? o.b : d.e;
+                if (lo >= hi) continue;
+                CK(cudaMemcpyPeerAsync(d.buf[cur] + (size_t)(lo - d.s) * rowC, d.dev, o.buf[cur] + (size_t)(lo - o.s) * rowC,
+                                       o.dev, (size_t)(hi - lo) * rowC * 4, d.st));
+            }
+        }
+        barrier();
+        for (SlabDev& d : sl_) {  // the window as an ordinary Column pass on its transpose
+            CK(cudaSetDevice(d.dev));
+            const int ws = d.e - d.s;
+            CK(launch_transpose(d.buf[cur], d.tmpT, ws, W_, C_, 1, d.st));
+            run_smooth(d.tmpT, d.gwinT, 1, ws, W_, C_, Cg_, &pcfg_, d.buf[cur ^ 1], first ? d.err : nullptr, d.st, true);
+        }
+    }
+
+    static void init_pool_once_dev(int dev) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ULLONG_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
+
+    int W_, H_, C_, Cg_;
+    sgwls_b200_config cfg_, pcfg_;
+    WeightDev wd_;
+    int G_;
+    size_t recn_ = 0;
+    std::vector<SlabDev> sl_;
+};
+
+// devices / ndev -> the device list; ndev <= 0: SGWLS_B200_DEVICES ("0,1,...") or device 0
+std::vector<int> device_list(const int* devices, int ndev) {
+    std::vector<int> v;
+    if (ndev > 0) {
+        if (!devices) throw Fail{SGWLS_B200_EINVAL, "sgwls_b200: null device list"};
+        v.assign(devices, devices + ndev);
+    } else if (const char* e = std::getenv("SGWLS_B200_DEVICES")) {
+        std::string s(e);
+        size_t i = 0;
+        while (i < s.size()) {
+            size_t j = s.find(',', i);
+            if (j == std::string::npos) j = s.size();
+            if (j > i) v.push_back(std::atoi(s.substr(i, j - i).c_str()));
+            i = j + 1;
+        }
+    }
+    if (v.empty()) v.push_back(0);
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    for (int d : v)
+        if (d < 0 || d >= n) throw Fail{SGWLS_B200_EINVAL, "sgwls_b200: device " + std::to_string(d) + " does not exist"};
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sgwls_b200_smooth_multi(const float* target, int width, int height, int channels, const float* guidance,
+                            int gch, const sgwls_b200_config* cfg, const int* devices, int ndev, float* out,
+                            char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::string msg;
+        int rc = validate_cfg(cfg, msg);
+        if (rc) throw Fail{rc, msg};
+        rc = check_shape(1, width, height, channels, gch, msg);
+        if (rc) throw Fail{rc, msg};
+        require_device();
+        DevGuard keep;
+        const std::vector<int> devs = device_list(devices, ndev);
+        // one device, or a geometry the slab mode does not cover (clipped bands,
+        // r > 4, 2/4 guidance channels, too few rows per slab): the whole image on
+        // the first device
+        const AxisPlan ap = plan_axis(height, width, channels, gch, cfg->r, cfg->tau, 1);
+        const int G = (int)devs.size();
+        bool slabs_ok = G > 1 && ap.fast && width >= 2 * cfg->r + 1;
+        auto slab_start = [&](int g) { return g >= G ? height : 2 * (int)(((long long)g * height) / (2LL * G)); };
+        for (int g = 0; g < G && slabs_ok; ++g) slabs_ok = slab_start(g + 1) > slab_start(g);  // non-empty slabs
+        if (!slabs_ok) {
+            CK(cudaSetDevice(devs[0]));
+            smooth_host(target, guidance, 1, width, height, channels, gch, cfg, out);
+            return;
+        }
+        MultiSlab ms(devs.data(), G, width, height, channels, gch, cfg);
+        ms.init();
+        ms.run(target, guidance, out);
+    });
+}
+
+// `batch` independent interpolate_sparse pairs split over the devices (each
+// device runs a contiguous share of the pairs on its own host thread).
+int sgwls_b200_interpolate_sparse_batch_multi(const float* values, const float* masks, const float* guidances,
+                                              int batch, int width, int height, int channels, int gch,
+                                              const sgwls_b200_config* cfg, const int* devices, int ndev, float* out,
+                                              float* undefined_mask, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        require_device();
+        DevGuard keep;
+        std::vector<int> devs = device_list(devices, ndev);
+        if (batch < 1) throw Fail{SGWLS_B200_EINVAL, "smooth: empty target"};
+        if ((int)devs.size() > batch) devs.resize(batch);
+        const int G = (int)devs.size();
+        const size_t npx = (size_t)width * height;
+        std::vector<int> rcs(G, 0);
+        std::vector<std::string> msgs(G);
+        std::vector<std::thread> th;
+        for (int g = 0; g < G; ++g) {
+            th.emplace_back([&, g] {
+                const int b0 = (int)((long long)g * batch / G), b1 = (int)((long long)(g + 1) * batch / G);
+                char e2[512] = {0};
+                if (cudaSetDevice(devs[g]) != cudaSuccess) {
+                    rcs[g] = SGWLS_B200_ECUDA;
+                    msgs[g] = "sgwls_b200: cannot select device " + std::to_string(devs[g]);
+                    return;
+                }
+                rcs[g] = sgwls_b200_interpolate_sparse_batch(
+                    values + b0 * npx * channels, masks + b0 * npx, guidances + b0 * npx * gch, b1 - b0, width, height,
+                    channels, gch, cfg, out + b0 * npx * channels, undefined_mask ? undefined_mask + b0 * npx : nullptr,
+                    e2, sizeof e2);
+                msgs[g] = e2;
+            });
+        }
+        for (auto& t : th) t.join();
+        for (int g = 0; g < G; ++g)  // the first failing share in batch order, like the serial loop
+            if (rcs[g]) throw Fail{rcs[g], msgs[g]};
     });
 }
 

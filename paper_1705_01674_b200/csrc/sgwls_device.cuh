@@ -62,6 +62,10 @@ struct PassGeom {
     // in a separator shared with the next slab).  0/0 for an ordinary pass.
     int has_prev, has_next;
     int row0;               // global row of local row 0 (error positions)
+    // Split input (tiled path, interpolate_sparse's first pass): the pass input
+    // is C-1 value channels at `src` plus the mask as channel C-1 at msk
+    // (proj/src/smoother.cpp:146-147 smooths both) -- no packed copy.
+    const float* msk;
 };
 
 __host__ __device__ __forceinline__ unsigned tau_multiplier(int tau) {

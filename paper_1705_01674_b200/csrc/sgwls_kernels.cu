@@ -117,8 +117,13 @@ __global__ void k_ratio(const float* __restrict__ packed, float* __restrict__ ou
 // violating pixel index (mask not 0/1, or value nonzero where mask is 0),
 // status[1] = number of pixels with mask == 1 (saturating).
 __global__ void k_validate_sparse(const float* __restrict__ values, const float* __restrict__ mask, long long npx,
-                                  int C, unsigned long long* status) {
+                                  int C, int batch, unsigned long long* status) {
     const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const int bi = blockIdx.y;  // pair
+    values += (long long)bi * npx * C;
+    mask += (long long)bi * npx;
+    unsigned long long* any_w = status + batch + bi;
+    status += bi;
     bool any = false;
     if (i < npx) {
         const float mv = mask[i];
@@ -130,7 +135,7 @@ __global__ void k_validate_sparse(const float* __restrict__ values, const float*
                 if (values[i * C + c] != 0.f) bad = true;
         if (bad) atomicMin(&status[0], (unsigned long long)i);
     }
-    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&status[1], 1ull);
+    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(any_w, 1ull);
 }
 
 // =========================================================== dispatch
@@ -202,9 +207,11 @@ cudaError_t launch_ratio(const float* packed, float* out, float* und, long long 
     return cudaGetLastError();
 }
 
-cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C,
+cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C, int batch,
                                    unsigned long long* status, cudaStream_t st) {
-    k_validate_sparse<<<(unsigned)((npx + 255) / 256), 256, 0, st>>>(values, mask, npx, C, status);
+    ProfScope ps("validate_sparse", st);
+    k_validate_sparse<<<dim3((unsigned)((npx + 255) / 256), (unsigned)batch), 256, 0, st>>>(values, mask, npx, C, batch,
+                                                                                           status);
     return cudaGetLastError();
 }
 

@@ -29,6 +29,11 @@ struct PassLaunch {
     float* maps = nullptr;    // tiled path: affine map of every inner chunk separator of a KA tile
                               // (KA -> KB), [chunk][field][line], map_floats(r, C) fields
     int nwa = 8;              // tiled path: chunks per KA tile (super-chunk)
+    // tiled path, interpolate_sparse's last pass: out = C-1 channels num / den
+    // (0 where den < ratio_floor), und = undefined mask (or nullptr)
+    int ratio = 0;
+    float ratio_floor = 0.f;
+    float* und = nullptr;
     // tiled path, row-slab mode (geom.has_prev / has_next, sgwls_tile.cuh):
     // 1 = phase A (KA, then this slab's record -> slabrec), 2 = phase B (slabrec
     // = all nslab records; separators, KC, KB); z and sep then carry one slot in
@@ -50,7 +55,9 @@ cudaError_t launch_pack_sparse(const float* values, const float* mask, float* pa
                                cudaStream_t st);
 cudaError_t launch_ratio(const float* packed, float* out, float* und, long long npx, int C, float floor_,
                          cudaStream_t st);
-cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C,
+// batch pairs: status[b] = min violating pixel of pair b (~0 if none),
+// status[batch + b] = nonzero if pair b has a mask pixel == 1
+cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C, int batch,
                                    unsigned long long* status, cudaStream_t st);
 
 // application-pipeline stages (sgwls_apps.cu, proj/src/apps.cpp)

@@ -154,8 +154,9 @@ struct ChunkIn {
 
 template <int R, int C, int CG, int RW, int WK, bool FULLC>
 __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
-                                             const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
-                                             int lo, int y0, int nrows, unsigned long long* err, int line) {
+                                             const float* __restrict__ Msk, const float* __restrict__ G,
+                                             const PassGeom& g, const WeightDev& W, int lo, int y0, int nrows,
+                                             unsigned long long* err, int line) {
     constexpr int M = 2 * R + 1, K = RW * M;
     float gp[K][CG];
     float gprev[R][CG];  // positions y0*M - R .. y0*M - 1 (last R of row y0-1)
@@ -178,9 +179,14 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
     // serpentine reversal of odd rows (proj/src/snake.cpp:21-49) is applied to
     // the values.  With an even RW the row parity is compile-time (chunks start
     // on even rows).  FULLC: every row of the chunk exists (no predicates).
-    const float* rowF = F + ((long long)y0 * g.Wl + lo) * C;
-    const float* rowG = G + ((long long)y0 * g.Wl + lo) * CG;
-    const long long stF = (long long)g.Wl * C, stG = (long long)g.Wl * CG;
+    // split input: F holds C-1 value channels, channel C-1 comes from the mask
+    const bool split = C > 1 && g.msk != nullptr;
+    constexpr int CV = C > 1 ? C - 1 : 1;
+    const long long px0 = (long long)y0 * g.Wl + lo;
+    const float* rowF = F + px0 * (split ? CV : C);
+    const float* rowM = split ? Msk + px0 : nullptr;
+    const float* rowG = G + px0 * CG;
+    const long long stF = (long long)g.Wl * (split ? CV : C), stG = (long long)g.Wl * CG;
 #pragma unroll
     for (int rr = 0; rr < RW; ++rr) {
         const bool valid = FULLC || rr < nrows;
@@ -190,7 +196,9 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
         for (int jj = 0; jj < M; ++jj) {
             if (valid) {
 #pragma unroll
-                for (int c = 0; c < C; ++c) vf[jj][c] = __ldg(rowF + jj * C + c);
+                for (int c = 0; c < C; ++c)
+                    vf[jj][c] = !split ? __ldg(rowF + jj * C + c)
+                                       : (c < C - 1 ? __ldg(rowF + jj * CV + c) : __ldg(rowM + jj));
 #pragma unroll
                 for (int c = 0; c < CG; ++c) vg[jj][c] = __ldg(rowG + jj * CG + c);
             } else {
@@ -210,6 +218,7 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
         }
         rowF += stF;
         rowG += stG;
+        if (split) rowM += g.Wl;
     }
     // edge weights (proj/src/weights.cpp:48-71); spatial factor index is compile-time.
     // A NaN weight (NaN guidance) is the reference's "non-positive pivot" failure:
@@ -259,21 +268,25 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
 template <int R, int C, int CG, int RW>
 __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
                                            const float* __restrict__ G, const PassGeom& g, const WeightDev& W,
-                                           int lo, int y0, int nrows, unsigned long long* err, int line) {
+                                           int lo, int y0, int nrows, unsigned long long* err, int line, int img) {
+    // image img of the pass input (split: C-1 value channels + the mask)
+    const long long npx = (long long)g.Hl * g.Wl;
+    const float* Msk = (C > 1 && g.msk != nullptr) ? g.msk + img * npx : nullptr;
+    F += img * (Msk ? npx * (C > 1 ? C - 1 : 1) : g.img_stride);
 #ifndef SGWLS_NO_FULL_LOAD
     if (W.kind == 1) {
         if (nrows == RW)
-            load_chunk_k<R, C, CG, RW, 1, true>(in, F, G, g, W, lo, y0, nrows, err, line);
+            load_chunk_k<R, C, CG, RW, 1, true>(in, F, Msk, G, g, W, lo, y0, nrows, err, line);
         else
-            load_chunk_k<R, C, CG, RW, 1, false>(in, F, G, g, W, lo, y0, nrows, err, line);
+            load_chunk_k<R, C, CG, RW, 1, false>(in, F, Msk, G, g, W, lo, y0, nrows, err, line);
     } else {
-        load_chunk_k<R, C, CG, RW, 0, false>(in, F, G, g, W, lo, y0, nrows, err, line);
+        load_chunk_k<R, C, CG, RW, 0, false>(in, F, Msk, G, g, W, lo, y0, nrows, err, line);
     }
 #else
     if (W.kind == 1)
         load_chunk_k<R, C, CG, RW, 1, false>(in, F, G, g, W, lo, y0, nrows, err, line);
     else
-        load_chunk_k<R, C, CG, RW, 0, false>(in, F, G, g, W, lo, y0, nrows, err, line);
+        load_chunk_k<R, C, CG, RW, 0, false>(in, F, Msk, G, g, W, lo, y0, nrows, err, line);
 #endif
 }
 
@@ -671,7 +684,8 @@ __device__ __forceinline__ void reduce_super(const float* recs, long long rs, lo
 // records (the former KC launch) and no record round trip through HBM.
 template <int R, int C>
 __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int nw, bool first_super,
-                                                 bool last_super, float* out, long long os, float* bsm) {
+                                                 bool last_super, float* out, long long os, float* bsm,
+                                                 int cs = 32) {
     using RL = Rec<R, C>;
     constexpr int RSM = RL::RSM;
     auto bsrow = [&](int s, int mm) { return bsm + (s * R + mm) * RSM * 32; };
@@ -689,8 +703,8 @@ __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int 
     }
     const int nblk = last_super ? nw - 1 : nw;
     for (int s = 0; s < nblk; ++s) {
-        const float* t = recs + s * 32;
-        const float* h = recs + (s + 1) * 32;
+        const float* t = recs + s * cs;
+        const float* h = recs + (s + 1) * cs;
         enter_block<R, C, true>(w, t, h, rs, s < nw - 1, s > 0, s > 0 || !first_super);
         if (s > 0) {
 #pragma unroll
@@ -724,6 +738,29 @@ __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int 
             out[(RL::HE + q) * os] = w.he[q];
 #pragma unroll
             for (int c = 0; c < C; ++c) out[(RL::HG + q * C + c) * os] = w.hg[q][c];
+        }
+    }
+}
+
+// Value of one eliminated separator from its back-substitution rows (R rows of
+// RSM fields at bs[f*32], as reduce_super_fwd stores them) and the known
+// separators either side: zL (spike side) and zR (the window's hi block).
+template <int R, int C>
+__device__ __forceinline__ void solve_from_bs(const float* bs, const float (&zL)[R][C], const float (&zR)[R][C],
+                                              float (&x)[R][C]) {
+    constexpr int RSM = Rec<R, C>::RSM;
+#pragma unroll
+    for (int mm = R - 1; mm >= 0; --mm) {
+        const float* o = bs + mm * RSM * 32;
+#pragma unroll
+        for (int c = 0; c < C; ++c) {
+            float v = o[(2 * R - 1 + c) * 32];
+#pragma unroll
+            for (int i = mm + 1; i < 2 * R; ++i)
+                v = fmaf(o[(i - mm - 1) * 32], (i < R) ? x[i < R ? i : 0][c] : zR[i >= R ? i - R : 0][c], v);
+#pragma unroll
+            for (int q = 0; q < R; ++q) v = fmaf(o[(2 * R - 1 + C + q) * 32], zL[q][c], v);
+            x[mm][c] = v;
         }
     }
 }
@@ -873,13 +910,41 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     if (w < NGa && ok)
         reduce_super<R, C, (R >= SGWLS_REC_PF_MINR)>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
     __syncthreads();
-    float z0[R][C];
+    // level 2 as a binary tree over the NGa group records: pairwise merges up
+    // (segment [a, a+span) absorbs [a+span, a+2span), eliminating group
+    // separator a+span-1, whose back-substitution rows stay in shared memory),
+    // then the eliminated separators top-down from their segments' two ends:
+    // 2 log2(NG) dependent steps instead of 2 NG
+    int top = 1;
+    while (top < NGa) top *= 2;
+    for (int span = 1; span < NGa; span *= 2) {
+        const int a = w * 2 * span;
+        if (ok && a + span < NGa)
+            reduce_super_fwd<R, C>(grec + a * 32 + lane, rsG, 2, a == 0, a + 2 * span >= NGa, grec + a * 32 + lane, rsG,
+                                   bsg + (a + span - 1) * R * RL::RSM * 32 + lane, span * 32);
+        __syncthreads();
+    }
+    for (int span = top / 2; span >= 1; span /= 2) {
+        const int a = w * 2 * span;
+        if (ok && a + span < NGa) {
+            float zL[R][C], zR[R][C], x[R][C];
+            const bool hl = a > 0, hr = a + 2 * span < NGa;
 #pragma unroll
-    for (int q = 0; q < R; ++q)
+            for (int q = 0; q < R; ++q)
 #pragma unroll
-        for (int c = 0; c < C; ++c) z0[q][c] = 0.f;
-    if (w == 0 && ok && NGa > 1) solve_inner<R, C>(grec + lane, rsG, 32, NGa, false, z0, false, z0, zg + lane, 32, bsg + lane, 32);
-    __syncthreads();
+                for (int c = 0; c < C; ++c) {
+                    zL[q][c] = hl ? zg[(((a - 1) * R + q) * C + c) * 32 + lane] : 0.f;
+                    zR[q][c] = hr ? zg[(((a + 2 * span - 1) * R + q) * C + c) * 32 + lane] : 0.f;
+                }
+            const int k = a + span - 1;
+            solve_from_bs<R, C>(bsg + k * R * RL::RSM * 32 + lane, zL, zR, x);
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) zg[((k * R + q) * C + c) * 32 + lane] = x[q][c];
+        }
+        __syncthreads();
+    }
     if (w < NGa && ok) {
         const bool has_l = w > 0, has_r = w < NGa - 1;
         float zL[R][C], zR[R][C];
@@ -914,7 +979,7 @@ __global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __
 template <int R, int C>
 __host__ inline size_t k2_tree_smem(int NG) {
     using RL = Rec<R, C>;
-    return ((size_t)RL::REC * (NG * 32 + 1) + (size_t)NG * R * C * 32 + (size_t)NG * R * RL::RS * 32) * sizeof(float);
+    return ((size_t)RL::REC * (NG * 32 + 1) + (size_t)NG * R * C * 32 + (size_t)NG * R * RL::RSM * 32) * sizeof(float);
 }
 
 // ===================================================================== KA
@@ -959,8 +1024,7 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
         const int y0 = j * RW;
         const int nrows = min(RW, g.Hl - y0);
         ChunkIn<R, C, CG, RW> in;
-        load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows,
-                                 nullptr, L);
+        load_chunk<R, C, CG, RW>(in, src, guid + img * g.gimg_stride, g, W, lo, y0, nrows, nullptr, L, img);
         chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0 || g.has_prev, j == g.P - 1 && !g.has_next, nrows * M, rec,
                                           rs);
     }
@@ -1186,6 +1250,12 @@ struct TileOut {
     int nwa;        // chunks per KA tile (the tiles KA's separator maps refer to)
     int psa;        // KA tiles per band
     int early;      // the predecessor is a K2 launch (it waited for KA): KA's maps may be read before the wait
+    // interpolate_sparse's last pass (proj/src/smoother.cpp:149-161): channel C-1
+    // is the smoothed mask d; out gets C-1 channels num/d (0 where d < floor)
+    // and und[pixel] = (d < floor), instead of the C smoothed channels
+    int ratio;
+    float floor_;
+    float* und;
 };
 
 // 1/n correctly rounded (what 1.0f / n gives) for the band count of a column, n <= 2r + 2 <= 10
@@ -1483,8 +1553,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     };
     if (to.early) fetch_maps();
     if (active)
-        load_chunk<R, C, CG, RW>(in, src + img * g.img_stride, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err,
-                                 L);
+        load_chunk<R, C, CG, RW>(in, src, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err, L, img);
     pdl_wait();  // super-separators (K2), maps (KA)
     pdl_trigger();
     if (!to.early) fetch_maps();
@@ -1558,7 +1627,8 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
 #ifndef SGWLS_NO_DIRECT
     // measured on B200: c1 +8.5 %, c3 +1.8 %, c5 +0.6 %; c4 (2 channels, float2 runs) -4.7 %, so
     // only for one channel or full float4 runs
-    const bool direct = shfl_avg && to.transpose_out && (C == 1 || DVEC == 4) && ((long long)g.Hl * C) % DVEC == 0 &&
+    const bool direct = shfl_avg && !to.ratio && to.transpose_out && (C == 1 || DVEC == 4) &&
+                        ((long long)g.Hl * C) % DVEC == 0 &&
                         (reinterpret_cast<uintptr_t>(oi) & (DVEC * 4 - 1)) == 0;
 #else
     const bool direct = false;
@@ -1621,7 +1691,24 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     }
     // ---- 5. owned columns -> global.  Transposed layout: each owned column is
     //         TR*C contiguous floats of the output.
-    if (colmaj && n >= 64) {  // >= 256-byte runs: one bulk (TMA) shared->global copy per owned column
+    if (to.ratio) {  // fused Eq. 21 ratio with the reference floor, one thread per (column, row)
+        constexpr int CV = C > 1 ? C - 1 : 1;
+        const long long npx = (long long)g.Hl * g.Wl;
+        float* ov = to.out + img * npx * CV;
+        float* ou = to.und ? to.und + img * npx : nullptr;
+        for (int idx = tid; idx < ncol * TR; idx += NT) {
+            const int xl = idx / TR, y = idx - xl * TR;
+            if (inv_col[xl] <= 0.f) continue;
+            const float* tp = tl + xl * sx + y * sy;
+            const float d = tp[C - 1];
+            const bool undef = d < to.floor_;
+            const long long px = to.transpose_out ? (long long)(xa + xl) * g.Hl + Y0 + y
+                                                  : (long long)(Y0 + y) * g.Wl + xa + xl;
+#pragma unroll
+            for (int c = 0; c < CV; ++c) ov[px * CV + c] = undef ? 0.f : tp[c] / d;
+            if (ou) ou[px] = undef ? 1.f : 0.f;
+        }
+    } else if (colmaj && n >= 64) {  // >= 256-byte runs: one bulk (TMA) shared->global copy per owned column
         bool issued = false;
         for (int xl = tid; xl < ncol; xl += NT) {
             if (inv_col[xl] > 0.f) {
@@ -1764,7 +1851,8 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
         // triggering) or, with a single KA tile per band, KA itself
         const bool early = slab || PSA > 1;
-        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0};
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, pl.ratio, pl.ratio_floor,
+                   pl.und};
         const dim3 kgrid(pl.ncta, PB, g.batch);
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

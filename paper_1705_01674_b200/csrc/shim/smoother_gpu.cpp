@@ -66,8 +66,11 @@ Image smooth(const Image& target, const Image& guidance, const SmoothConfig& cfg
     std::vector<float> o(t.size());
     const sgwls_b200_config c = to_c(cfg);
     char err[512];
-    check(sgwls_b200_smooth(t.data(), target.width, target.height, target.channels, g.data(), guidance.channels,
-                            &c, o.data(), err, sizeof err),
+    // ndev = 0: the devices listed in SGWLS_B200_DEVICES (one image in row slabs
+    // across them), else device 0 -- the reference's callers reach multi-GPU
+    // without a code change, like its own cfg.threads knob
+    check(sgwls_b200_smooth_multi(t.data(), target.width, target.height, target.channels, g.data(),
+                                  guidance.channels, &c, nullptr, 0, o.data(), err, sizeof err),
           err);
     Image out(target.width, target.height, target.channels);
     for (std::size_t i = 0; i < o.size(); ++i) out.data[i] = o[i];

@@ -183,8 +183,8 @@ class SlabSmoother:
         n = 0
         for p in range(self.T):
             for g in self.ex.local:
-                if ((self.fa + p) & 1) == 0:  # KA, slab reduce | slab solve, [KC,] KB
-                    n += 4 + (1 if self.cfg.r >= 2 else 0)
+                if ((self.fa + p) & 1) == 0:  # KA, slab reduce | slab solve, KB
+                    n += 4
                 else:  # window transpose + one pass
                     n += 1 + kernel_launches(self.win[g].width, self.W, self.C, self.Cg, 1, False, self.pcfg)
         return n

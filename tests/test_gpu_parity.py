@@ -87,6 +87,44 @@ def test_interpolate_sparse_matches_oracle(port):
     assert (gund == wund).all()
 
 
+SPARSE_CASES = [
+    # (h, w, C values, r, tau, T, first axis): first pass reads values + mask
+    # unpacked and the last pass writes the ratio (tiled path), or the pack /
+    # ratio kernels (first axis Row: pack; clipped geometry: generic path)
+    (90, 70, 1, 2, 2, 4, 0),
+    (90, 70, 2, 1, 3, 3, 0),   # last pass a column pass: ratio untransposed
+    (64, 80, 3, 4, 2, 1, 0),   # T = 1: split input and ratio in the same pass
+    (75, 66, 1, 2, 3, 4, 1),   # first axis Row: packed input, fused ratio
+    (40, 4, 1, 2, 1, 2, 0),    # width < 2r+1: generic path, pack + ratio kernels
+]
+
+
+@pytest.mark.parametrize("case", SPARSE_CASES, ids=[f"{c[0]}x{c[1]}c{c[2]}_r{c[3]}t{c[4]}T{c[5]}a{c[6]}"
+                                                    for c in SPARSE_CASES])
+def test_interpolate_sparse_paths(case, port):
+    import torch
+
+    h, w, c, r, tau, T, fa = case
+    rng = np.random.default_rng(sum(case))
+    g = _piecewise(rng, h, w, 1)[:, :, 0]
+    mask = (rng.uniform(0, 1, (h, w)) < 1 / 8).astype(np.float32)
+    mask[0, 0] = 1.0
+    vals = (mask[:, :, None] * rng.uniform(0.2, 1, (h, w, c))).astype(np.float32)
+    cfg = _cfg(400.0, r, tau, T, 1, fa, sigma_r=0.05)
+    want, wund = port.interpolate_sparse(vals, mask, g, cfg)
+    got, gund = S.interpolate_sparse(S.SparseField(vals, mask), g, cfg, return_undefined=True)
+    assert np.abs(got - want.reshape(got.shape)).max() <= TOL
+    assert (gund == wund).all()
+    # device batch form (2 pairs) = host form, bit for bit
+    dv = torch.from_numpy(np.stack([vals, vals])).cuda()
+    dm = torch.from_numpy(np.stack([mask, mask])).cuda()
+    dg = torch.from_numpy(np.stack([g, g])).cuda()
+    und = torch.empty_like(dm)
+    out = S.interpolate_sparse_device(dv, dm, dg, cfg, undefined=und, validate=True, sync=True)
+    assert np.array_equal(out[1].cpu().numpy(), got.reshape(h, w, c))
+    assert np.array_equal(und[0].cpu().numpy(), gund)
+
+
 def test_batch_equals_single():
     rng = np.random.default_rng(9)
     ts = np.stack([_piecewise(rng, 50, 40, 1)[:, :, 0] for _ in range(3)])
