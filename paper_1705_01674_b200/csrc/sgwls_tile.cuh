@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <type_traits>
 #include <utility>
 
 #include "sgwls_device.cuh"
@@ -264,6 +265,97 @@ __device__ __forceinline__ void load_chunk_k(ChunkIn<R, C, CG, RW>& in, const fl
     }
 }
 
+// Lazy form (KA): the chunk's samples and guidance only; each edge weight is
+// computed where the elimination consumes it (fewer live registers, MUFU work
+// interleaved with the dependent elimination chain).
+template <int R, int C, int CG, int RW>
+struct ChunkInL {
+    static constexpr int M = 2 * R + 1, K = RW * M;
+    float f[K][C];
+    float gp[K][CG];
+    float gprev[R][CG];
+};
+
+template <int R, int C, int CG, int RW, bool FULLC>
+__device__ __forceinline__ void load_chunk_lazy(ChunkInL<R, C, CG, RW>& in, const float* __restrict__ F,
+                                                const float* __restrict__ Msk, const float* __restrict__ G,
+                                                const PassGeom& g, int lo, int y0, int nrows) {
+    constexpr int M = 2 * R + 1;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int jj = M - R + i;
+        const int y = y0 - 1;
+        if (y >= 0 || g.has_prev) {
+            const int co = (y & 1) ? (M - 1 - jj) : jj;
+            const float* p = G + ((long long)y * g.Wl + lo + co) * CG;
+#pragma unroll
+            for (int c = 0; c < CG; ++c) in.gprev[i][c] = __ldg(p + c);
+        } else {
+#pragma unroll
+            for (int c = 0; c < CG; ++c) in.gprev[i][c] = 0.f;
+        }
+    }
+    const bool split = C > 1 && Msk != nullptr;
+    constexpr int CV = C > 1 ? C - 1 : 1;
+    const long long px0 = (long long)y0 * g.Wl + lo;
+    const float* rowF = F + px0 * (split ? CV : C);
+    const float* rowM = split ? Msk + px0 : nullptr;
+    const float* rowG = G + px0 * CG;
+    const long long stF = (long long)g.Wl * (split ? CV : C), stG = (long long)g.Wl * CG;
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+        const bool valid = FULLC || rr < nrows;
+        const bool odd = (RW % 2 == 0) ? ((rr & 1) != 0) : (((y0 + rr) & 1) != 0);
+        float vf[M][C], vg[M][CG];
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+#pragma unroll
+            for (int c = 0; c < C; ++c)
+                vf[jj][c] = !valid ? 0.f
+                                   : (!split ? __ldg(rowF + jj * C + c)
+                                             : (c < C - 1 ? __ldg(rowF + jj * CV + c) : __ldg(rowM + jj)));
+#pragma unroll
+            for (int c = 0; c < CG; ++c) vg[jj][c] = valid ? __ldg(rowG + jj * CG + c) : 0.f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            const int k = rr * M + jj;
+#pragma unroll
+            for (int c = 0; c < C; ++c) in.f[k][c] = odd ? vf[M - 1 - jj][c] : vf[jj][c];
+#pragma unroll
+            for (int c = 0; c < CG; ++c) in.gp[k][c] = odd ? vg[M - 1 - jj][c] : vg[jj][c];
+        }
+        rowF += stF;
+        rowG += stG;
+        if (split) rowM += g.Wl;
+    }
+}
+
+// lambda * w of edge (k - t, k) of a lazily loaded chunk (k, t compile-time after unrolling)
+template <int R, int C, int CG, int RW, int WK>
+struct LazyWeights {
+    const ChunkInL<R, C, CG, RW>& in;
+    const WeightDev& W;
+    __device__ __forceinline__ float operator()(int k, int t) const {
+        constexpr int K = RW * (2 * R + 1);
+        float r2 = 0.f;
+#pragma unroll
+        for (int c = 0; c < CG; ++c) {
+            const float other = (k - t >= 0) ? in.gp[cl(k - t, K)][c] : in.gprev[cl(k - t + R, R)][c];
+            const float d = in.gp[cl(k, K)][c] - other;
+            r2 = fmaf(d, d, r2);
+        }
+        return guidance_lweight_k<WK>(W, r2, edge_d2(k % (2 * R + 1), t));
+    }
+};
+template <int R, int C, int CG, int RW>
+struct EagerWeights {
+    const ChunkIn<R, C, CG, RW>& in;
+    __device__ __forceinline__ float operator()(int k, int t) const {
+        return in.w[cl(k, RW * (2 * R + 1))][t - 1];
+    }
+};
+
 // One uniform branch per chunk on the weight kind instead of one per edge.
 template <int R, int C, int CG, int RW>
 __device__ __forceinline__ void load_chunk(ChunkIn<R, C, CG, RW>& in, const float* __restrict__ F,
@@ -388,9 +480,9 @@ struct Win {
 // FULL: the chunk has all RW rows (every chunk but possibly the band's last):
 // the position loop is then free of runtime predicates, so the window shifts
 // compile to register renames.
-template <int R, int C, int CG, int RW, bool FULL>
-__device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                         bool last, int kv, float* rec, int rs) {
+template <int R, int C, int CG, int RW, bool FULL, class IN, class WF>
+__device__ __forceinline__ void chunk_spike_forward_impl(const IN& in, const WF& lwf, bool has_left, bool last, int kv,
+                                                         float* rec, int rs) {
     using RL = Rec<R, C>;
     auto put = [&](int f, float v) { rec[f * rs] = v; };
     constexpr int K = RW * (2 * R + 1);
@@ -404,7 +496,7 @@ __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG,
             for (int c = 0; c < C; ++c) w.g[R][c] = in.f[k][c];
 #pragma unroll
             for (int t = 1; t <= R; ++t) {
-                const float lw = in.w[k][t - 1];
+                const float lw = lwf(k, t);
                 if (k - t >= 0) {
                     w.A[R - t][R] = lw;
                 } else if (has_left) {
@@ -447,13 +539,13 @@ __device__ __forceinline__ void chunk_spike_forward_impl(const ChunkIn<R, C, CG,
     }
 }
 
-template <int R, int C, int CG, int RW>
-__device__ __forceinline__ void chunk_spike_forward(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left,
-                                                    bool last, int kv, float* rec, int rs) {
+template <int R, int C, int CG, int RW, class IN, class WF>
+__device__ __forceinline__ void chunk_spike_forward(const IN& in, const WF& lwf, bool has_left, bool last, int kv,
+                                                    float* rec, int rs) {
     if (kv == RW * (2 * R + 1))
-        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lam, has_left, last, kv, rec, rs);
+        chunk_spike_forward_impl<R, C, CG, RW, true>(in, lwf, has_left, last, kv, rec, rs);
     else
-        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lam, has_left, last, kv, rec, rs);
+        chunk_spike_forward_impl<R, C, CG, RW, false>(in, lwf, has_left, last, kv, rec, rs);
 }
 
 // ---------------------------------------------- block window (separator level)
@@ -967,8 +1059,9 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     }
 }
 
-template <int R, int C>
-__global__ void __launch_bounds__(512) k2_tree(const PassGeom g, const float* __restrict__ rec,
+// MAXT: 512 threads (<= 128 registers) up to 16 groups; 1024 (<= 64) for 32
+template <int R, int C, int MAXT>
+__global__ void __launch_bounds__(MAXT) k2_tree(const PassGeom g, const float* __restrict__ rec,
                                                float* __restrict__ rsc, float* __restrict__ z) {
     extern __shared__ float sm[];
     pdl_wait();     // KA's records
@@ -994,12 +1087,25 @@ template <int R, int C, int CG>
 #define SGWLS_KA_MINB (R >= 2 ? 4 : 3)
 #endif
 #define SGWLS_KA_BOUNDS __launch_bounds__(256, SGWLS_KA_MINB)
-#ifndef SGWLS_KB_MINB
-// KB: <= 85 registers (measured +3% c5, +8% c4); <= 64 for one channel
-// once the averaging went to shuffles and direct stores (c5 +1.6 %, c3 +0.7 %; c4 -1 %)
-#define SGWLS_KB_MINB (C == 1 ? 4 : 3)
+// Edge weights computed where the elimination consumes them ("lazy") instead
+// of up front in registers, from this radius on: fewer live registers (KA: no
+// spills; KB: less spilling) and MUFU work interleaved with the dependent
+// elimination chain.  Measured on B200 (KA and KB lazy vs eager): c5 +13 %,
+// c4 +7 %, c3 +6 %; r = 1 (c1 -3 %, c2 -2 %: KB's weights then no longer
+// overlap the K2 wait) stays eager.
+#ifndef SGWLS_LAZY_MIN_R
+#define SGWLS_LAZY_MIN_R 2
 #endif
-#define SGWLS_KB_BOUNDS __launch_bounds__(256, SGWLS_KB_MINB)
+// KB register budget in 256-thread units: one channel 4 (<= 64 registers,
+// measured best with the shuffle averaging), several channels 3 (<= 85) for
+// r >= 2 and 2 (<= 128) for r = 1, whose wide C-channel windows spill badly at 85
+#ifndef SGWLS_KB_MINB1
+#define SGWLS_KB_MINB1 4
+#endif
+#ifndef SGWLS_KB_MINBC
+#define SGWLS_KB_MINBC (R == 1 ? 2 : 3)
+#endif
+#define SGWLS_KB_BOUNDS __launch_bounds__(256, (C == 1 ? SGWLS_KB_MINB1 : SGWLS_KB_MINBC))
 __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
                                                float* __restrict__ maps, const __grid_constant__ WeightDev W) {
@@ -1023,10 +1129,28 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
         const int lo = band_lo(g, b);
         const int y0 = j * RW;
         const int nrows = min(RW, g.Hl - y0);
+        const bool has_left = j > 0 || g.has_prev, lastc = j == g.P - 1 && !g.has_next;
+        if constexpr (R >= SGWLS_LAZY_MIN_R) {
+        // edge weights computed where the elimination consumes them
+        const long long npx = (long long)g.Hl * g.Wl;
+        const float* Msk = (C > 1 && g.msk != nullptr) ? g.msk + img * npx : nullptr;
+        const float* F = src + img * (Msk ? npx * (C > 1 ? C - 1 : 1) : g.img_stride);
+        ChunkInL<R, C, CG, RW> in;
+        if (nrows == RW)
+            load_chunk_lazy<R, C, CG, RW, true>(in, F, Msk, guid + img * g.gimg_stride, g, lo, y0, nrows);
+        else
+            load_chunk_lazy<R, C, CG, RW, false>(in, F, Msk, guid + img * g.gimg_stride, g, lo, y0, nrows);
+        if (W.kind == 1)
+            chunk_spike_forward<R, C, CG, RW>(in, LazyWeights<R, C, CG, RW, 1>{in, W}, has_left, lastc, nrows * M, rec,
+                                              rs);
+        else
+            chunk_spike_forward<R, C, CG, RW>(in, LazyWeights<R, C, CG, RW, 0>{in, W}, has_left, lastc, nrows * M, rec,
+                                              rs);
+        } else {
         ChunkIn<R, C, CG, RW> in;
         load_chunk<R, C, CG, RW>(in, src, guid + img * g.gimg_stride, g, W, lo, y0, nrows, nullptr, L, img);
-        chunk_spike_forward<R, C, CG, RW>(in, W.lam, j > 0 || g.has_prev, j == g.P - 1 && !g.has_next, nrows * M, rec,
-                                          rs);
+        chunk_spike_forward<R, C, CG, RW>(in, EagerWeights<R, C, CG, RW>{in}, has_left, lastc, nrows * M, rec, rs);
+        }
     }
     __syncthreads();
     const int PS = gridDim.y;  // = ceil(P / NW), the grid's tile dimension
@@ -1055,8 +1179,8 @@ __host__ inline size_t ka_smem(int NWA) {
 // couplings moved to the right-hand side, back substitution in registers.
 // FULL_INNER: full chunk that is not the band's last (kv = K, kend = K - R at
 // compile time); otherwise the general predicated form.
-template <int R, int C, int CG, int RW, bool FULL_INNER>
-__device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>& in, float lam, bool has_left, bool lastc,
+template <int R, int C, int CG, int RW, bool FULL_INNER, class IN, class WF>
+__device__ __forceinline__ void chunk_interior_solve(const IN& in, const WF& lwf, bool has_left, bool lastc,
                                                      int kv, int kend, const float (&zl)[R][C],
                                                      const float (&zr)[R][C], float (&cs)[RW * (2 * R + 1)][R],
                                                      float (&ys)[RW * (2 * R + 1)][C]) {
@@ -1092,7 +1216,7 @@ __device__ __forceinline__ void chunk_interior_solve(const ChunkIn<R, C, CG, RW>
                 const bool pleft = (k - t < 0);
                 const bool pright = kq && (k - t >= ks);
                 if (pright) continue;
-                const float lw = in.w[cl(k, K)][t - 1];
+                const float lw = lwf(k, t);
                 if (!kq && !pleft) {
                     w.A[R - t][R] = lw;
                 } else if (!kq && pleft) {
@@ -1487,7 +1611,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
 
     // ---- 1. chunk inputs and edge weights before the dependent-launch wait:
     //         the pass input was complete before KA began
-    ChunkIn<R, C, CG, RW> in;
+    std::conditional_t<(R >= SGWLS_LAZY_MIN_R), ChunkInL<R, C, CG, RW>, ChunkIn<R, C, CG, RW>> in;
     const int y0 = j * RW;
     const int nrows = active ? min(RW, g.Hl - y0) : 0;
     const int lo = active ? band_lo(g, b) : 0;
@@ -1552,8 +1676,45 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         cp_async_commit();
     };
     if (to.early) fetch_maps();
+    if constexpr (R >= SGWLS_LAZY_MIN_R) {
+    if (active) {
+        const long long npx = (long long)g.Hl * g.Wl;
+        const float* Msk = (C > 1 && g.msk != nullptr) ? g.msk + img * npx : nullptr;
+        const float* F = src + img * (Msk ? npx * (C > 1 ? C - 1 : 1) : g.img_stride);
+        if (nrows == RW)
+            load_chunk_lazy<R, C, CG, RW, true>(in, F, Msk, guid + img * g.gimg_stride, g, lo, y0, nrows);
+        else
+            load_chunk_lazy<R, C, CG, RW, false>(in, F, Msk, guid + img * g.gimg_stride, g, lo, y0, nrows);
+        if (err != nullptr) {  // NaN guidance: the reference's pivot failure (rare path locates it)
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int c = 0; c < CG; ++c) acc = fmaf(in.gp[k][c], 0.f, acc);
+#pragma unroll
+            for (int i = 0; i < R; ++i)
+#pragma unroll
+                for (int c = 0; c < CG; ++c) acc = fmaf(in.gprev[i][c], 0.f, acc);
+            if (!(acc >= 0.f)) {
+                const LazyWeights<R, C, CG, RW, 1> we{in, W};
+                const LazyWeights<R, C, CG, RW, 0> wf{in, W};
+                int bad = 0x7fffffff;
+#pragma unroll
+                for (int k = 0; k < K; ++k)
+#pragma unroll
+                    for (int t = 1; t <= R; ++t) {
+                        const float lw = W.kind == 1 ? we(k, t) : wf(k, t);
+                        const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0 || g.has_prev);
+                        bad = (!(lw >= 0.f) && exists) ? min(bad, (g.row0 + y0) * M + k - t) : bad;
+                    }
+                if (bad != 0x7fffffff) atomicMin(err, ((unsigned long long)(unsigned)L << 32) | (unsigned)bad);
+            }
+        }
+    }
+    } else {
     if (active)
         load_chunk<R, C, CG, RW>(in, src, guid + img * g.gimg_stride, g, W, lo, y0, nrows, err, L, img);
+    }
     pdl_wait();  // super-separators (K2), maps (KA)
     pdl_trigger();
     if (!to.early) fetch_maps();
@@ -1610,10 +1771,24 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         for (int c = 0; c < C; ++c) ys[p][c] = 0.f;
     }
     if (active) {
-        if (!lastc && kv == K)
-            chunk_interior_solve<R, C, CG, RW, true>(in, lam, has_left, lastc, kv, kend, zl, zr, cs, ys);
+        if constexpr (R >= SGWLS_LAZY_MIN_R) {
+        auto solve = [&](const auto& lwf) {
+            if (!lastc && kv == K)
+                chunk_interior_solve<R, C, CG, RW, true>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
+            else
+                chunk_interior_solve<R, C, CG, RW, false>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
+        };
+        if (W.kind == 1)
+            solve(LazyWeights<R, C, CG, RW, 1>{in, W});
         else
-            chunk_interior_solve<R, C, CG, RW, false>(in, lam, has_left, lastc, kv, kend, zl, zr, cs, ys);
+            solve(LazyWeights<R, C, CG, RW, 0>{in, W});
+        } else {
+        const EagerWeights<R, C, CG, RW> lwf{in};
+        if (!lastc && kv == K)
+            chunk_interior_solve<R, C, CG, RW, true>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
+        else
+            chunk_interior_solve<R, C, CG, RW, false>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
+        }
     }
     __syncthreads();
     // ---- 4. averaging into the shared output tile, fixed phase order
@@ -1832,15 +2007,18 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         static const int ng_env = [] {
             const char* v = std::getenv("SGWLS_K2_NG");  // schedule knob: warps (groups) of the K2 tree
             const int n = v ? std::atoi(v) : 0;
-            return n == 4 || n == 8 || n == 16 ? n : 0;
+            return n == 4 || n == 8 || n == 16 || n == 32 ? n : 0;
         }();
-        // measured on B200: 16 warps from 16 super records on (c2 +3 %), 8 below (c1)
-        const int NG = ng_env ? ng_env : (PSA >= 16 ? 16 : 8);
+        // measured on B200 (level 2 as a merge tree): 32 warps for the long
+        // reduced systems of r <= 2 (c5 +4 %), 16 from 16 super records on, 8 below (c1 +3 %)
+        int NG = ng_env ? ng_env : (PSA >= 128 && R <= 2 ? 32 : (PSA >= 20 ? 16 : 8));
+        if (R > 2 && NG > 16) NG = 16;  // 1024 threads hold only 64 registers
+        while (NG > 4 && k2_tree_smem<R, C>(NG) > 200 * 1024) NG /= 2;
         const size_t sm2 = k2_tree_smem<R, C>(NG);
-        e = cudaFuncSetAttribute(k2_tree<R, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
+        auto kern = NG > 16 ? k2_tree<R, C, 1024> : k2_tree<R, C, 512>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         if (e != cudaSuccess) return e;
-        e = launch_pdl(k2_tree<R, C>, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs,
-                       pl.z);
+        e = launch_pdl(kern, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs, pl.z);
         if (e != cudaSuccess) return e;
     }
     {
