@@ -166,7 +166,7 @@ cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st) {
 
 size_t rec_floats(int r, int C) { return (size_t)(r * (r - 1) + r * r + 2 * r + 2 * r * C); }
 size_t rs_floats(int r, int C) { return (size_t)(2 * r - 1 + C); }
-size_t map_floats(int r, int C) { return (size_t)(r * (C + 2 * r)); }
+size_t map_floats(int r, int C) { return (size_t)((r * (C + 2 * r) + 3) & ~3); }  // padded (Rec::MAPP)
 
 cudaError_t launch_transpose(const float* in, float* out, int H, int W, int C, int batch, cudaStream_t st) {
     dim3 grid((W + 31) / 32, (H + 31) / 32, batch);

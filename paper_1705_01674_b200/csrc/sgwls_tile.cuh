@@ -65,9 +65,10 @@ __device__ __forceinline__ void bulk_commit_and_wait_read() {
 // order this thread's generic-proxy shared-memory writes before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-// 4-byte asynchronous global -> shared copy (LDGSTS: no registers held while in flight)
-__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)), "l"(gsrc)
+// 16-byte asynchronous global -> shared copy (LDGSTS: no registers held while in flight)
+__device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
+                 "l"(gsrc)
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
@@ -115,6 +116,9 @@ struct Rec {
     // [value (C) | left super-separator zL (R) | right super-separator zR (R)]
     static constexpr int NB = C + 2 * R;
     static constexpr int MAPF = R * NB;
+    // global layout of the maps: [chunk][line][MAPP] (MAPF padded to whole
+    // 16-byte vectors: a lane's map is one run of MAPP/4 float4s)
+    static constexpr int MAPP = (MAPF + 3) & ~3;
 };
 
 __host__ __device__ constexpr int rows_per_chunk(int R, int C) { return tile_rows_per_chunk(R, C); }
@@ -861,8 +865,7 @@ __device__ __forceinline__ void solve_from_bs(const float* bs, const float (&zL)
 // zL component or zR component): the columns are independent, so the warps of
 // the KA tile share them.  x_{nw-1} is the right super-separator itself.
 template <int R, int C>
-__device__ __forceinline__ void maps_backward_column(const float* bsm, int nw, bool last_super, int b, float* maps,
-                                                     long long ms) {
+__device__ __forceinline__ void maps_backward_column(const float* bsm, int nw, bool last_super, int b, float* maps) {
     using RL = Rec<R, C>;
     constexpr int NB = RL::NB, RSM = RL::RSM;
     float xn[R];
@@ -880,10 +883,12 @@ __device__ __forceinline__ void maps_backward_column(const float* bsm, int nw, b
                 v = fmaf(o[(i - mm - 1) * 32], (i < R) ? xc[i < R ? i : 0] : xn[i >= R ? i - R : 0], v);
             xc[mm] = v;
         }
-        float* mo = maps + ((long long)s * RL::MAPF + b) * ms;
+        // staged in shared memory, [separator][field][lane] with a 33-float field
+        // pitch (conflict-free both ways); ka_tile writes the tile's maps out coalesced
+        float* mo = maps + (s * RL::MAPP + b) * 33;
 #pragma unroll
         for (int q = 0; q < R; ++q) {
-            mo[(long long)q * NB * ms] = xc[q];
+            mo[q * NB * 33] = xc[q];
             xn[q] = xc[q];
         }
     }
@@ -1077,7 +1082,6 @@ __host__ inline size_t k2_tree_smem(int NG) {
 
 // ===================================================================== KA
 
-template <int R, int C, int CG>
 // Register budgets (tuning variants override these): KA is held to 3 CTAs of
 // 256 threads per SM; KB keeps plain __launch_bounds__(256) (ptxas settles at
 // ~95-128 registers; tighter budgets spill and lose on B200).
@@ -1100,37 +1104,26 @@ template <int R, int C, int CG>
 // measured best with the shuffle averaging), several channels 3 (<= 85) for
 // r >= 2 and 2 (<= 128) for r = 1, whose wide C-channel windows spill badly at 85
 #ifndef SGWLS_KB_MINB1
-#define SGWLS_KB_MINB1 4
+#define SGWLS_KB_MINB1 3
 #endif
 #ifndef SGWLS_KB_MINBC
 #define SGWLS_KB_MINBC (R == 1 ? 2 : 3)
 #endif
 #define SGWLS_KB_BOUNDS __launch_bounds__(256, (C == 1 ? SGWLS_KB_MINB1 : SGWLS_KB_MINBC))
-__global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
-                                               const float* __restrict__ guid, float* __restrict__ srec,
-                                               float* __restrict__ maps, const __grid_constant__ WeightDev W) {
+// One chunk of KA: load (lazily weighted for r >= SGWLS_LAZY_MIN_R), spike-forward,
+// record -> shared memory (`rec`, field stride rs).
+template <int R, int C, int CG>
+__device__ __forceinline__ void ka_chunk(const PassGeom& g, const float* __restrict__ src,
+                                         const float* __restrict__ guid, const WeightDev& W, int L, int j, float* rec,
+                                         int rs) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1;
-    using RL = Rec<R, C>;
-    extern __shared__ float sm[];
-    const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
-    const int NL = g.nb * g.batch;
-    // grid: (line group, tile)
-    const int L = blockIdx.x * 32 + lane;
-    const int J = blockIdx.y;
-    const int j = J * NW + wid;
-    const int nw = min(NW, g.P - J * NW);
-    const int rs = NW * 32 + 1;  // smem record field stride
-    float* rec = sm + wid * 32 + lane;
-    pdl_wait();  // the pass input is the previous pass's output
-    pdl_trigger();
-    if (L < NL && wid < nw) {
-        const int img = g.batch == 1 ? 0 : L / g.nb, b = L - img * g.nb;  // no integer division for one image
-        const int lo = band_lo(g, b);
-        const int y0 = j * RW;
-        const int nrows = min(RW, g.Hl - y0);
-        const bool has_left = j > 0 || g.has_prev, lastc = j == g.P - 1 && !g.has_next;
-        if constexpr (R >= SGWLS_LAZY_MIN_R) {
+    const int img = g.batch == 1 ? 0 : L / g.nb, b = L - img * g.nb;  // no integer division for one image
+    const int lo = band_lo(g, b);
+    const int y0 = j * RW;
+    const int nrows = min(RW, g.Hl - y0);
+    const bool has_left = j > 0 || g.has_prev, lastc = j == g.P - 1 && !g.has_next;
+    if constexpr (R >= SGWLS_LAZY_MIN_R) {
         // edge weights computed where the elimination consumes them
         const long long npx = (long long)g.Hl * g.Wl;
         const float* Msk = (C > 1 && g.msk != nullptr) ? g.msk + img * npx : nullptr;
@@ -1146,32 +1139,76 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
         else
             chunk_spike_forward<R, C, CG, RW>(in, LazyWeights<R, C, CG, RW, 0>{in, W}, has_left, lastc, nrows * M, rec,
                                               rs);
-        } else {
+    } else {
         ChunkIn<R, C, CG, RW> in;
         load_chunk<R, C, CG, RW>(in, src, guid + img * g.gimg_stride, g, W, lo, y0, nrows, nullptr, L, img);
         chunk_spike_forward<R, C, CG, RW>(in, EagerWeights<R, C, CG, RW>{in}, has_left, lastc, nrows * M, rec, rs);
-        }
     }
+}
+
+// KA: one tile (32 bands x NW chunks) per CTA.  Every warp runs one chunk's
+// spike-forward; then warp 0 reduces the tile's chunk records (super-record
+// for K2 + the back-substitution rows) and the warps share the map columns.
+// (A persistent form -- a per-CTA queue of (tile, chunk) tasks whose last
+// warp reduces the tile -- was measured 2x slower on c5: the serial reduction
+// of one warp could not keep up with the chunks of the other fifteen.)
+template <int R, int C, int CG>
+__global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
+                                               const float* __restrict__ guid, float* __restrict__ srec,
+                                               float* __restrict__ maps, const __grid_constant__ WeightDev W) {
+    using RL = Rec<R, C>;
+    extern __shared__ float sm[];
+    const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
+    const int NL = g.nb * g.batch;
+    // grid: (line group, tile)
+    const int L = blockIdx.x * 32 + lane;
+    const int J = blockIdx.y;
+    const int nw = min(NW, g.P - J * NW);
+    const int rs = NW * 32 + 1;  // smem record field stride
+    pdl_wait();  // the pass input is the previous pass's output
+    pdl_trigger();
+    if (L < NL && wid < nw) ka_chunk<R, C, CG>(g, src, guid, W, L, J * NW + wid, sm + wid * 32 + lane, rs);
     __syncthreads();
     const int PS = gridDim.y;  // = ceil(P / NW), the grid's tile dimension
     const long long NLl = NL;
-    float* bsm = sm + RL::REC * rs + lane;
+    const int recs_fl = RL::REC * rs, stage_fl = (NW > 1 ? NW - 1 : 1) * RL::MAPP * 33;
+    float* bsm = sm + (recs_fl > stage_fl ? recs_fl : stage_fl) + lane;
     const bool last_super = J == PS - 1 && !g.has_next;
     if (wid == 0 && L < NL)  // super-record for K2, back-substitution rows
         reduce_super_fwd<R, C>(sm + lane, rs, nw, J == 0 && !g.has_prev, last_super,
                                srec + (long long)J * RL::REC * NLl + L, NLl, bsm);
     if (nw < 2) return;
     __syncthreads();
-    // the affine maps of the tile's inner separators for KB, one basis column per warp
+    // the affine maps of the tile's inner separators for KB, one basis column
+    // per warp, staged in shared memory (the record area is free by now) ...
+    float* mst = sm + lane;
     if (L < NL)
-        for (int b = wid; b < RL::NB; b += NW)
-            maps_backward_column<R, C>(bsm, nw, last_super, b, maps + (long long)J * NW * RL::MAPF * NLl + L, NLl);
+        for (int b = wid; b < RL::NB; b += NW) maps_backward_column<R, C>(bsm, nw, last_super, b, mst);
+    __syncthreads();
+    // ... and written out as whole 16-byte vectors: a separator's maps for the
+    // tile's 32 lines are one contiguous run of 32*MAPP floats ([chunk][line][MAPP])
+    constexpr int V = RL::MAPP / 4;  // float4 per line
+    const int nv = (nw - 1) * 32 * V;
+    const int ngl = min(32, NL - (int)blockIdx.x * 32);  // lines of this group
+    for (int v = wid * 32 + lane; v < nv; v += NW * 32) {
+        const int sep = v / (32 * V), rem = v - sep * 32 * V, ln = rem / V, f = (rem - ln * V) * 4;
+        if (ln >= ngl) continue;
+        const float* src4 = sm + (sep * RL::MAPP + f) * 33 + ln;
+        float4 o;
+        o.x = src4[0];
+        o.y = f + 1 < RL::MAPF ? src4[33] : 0.f;
+        o.z = f + 2 < RL::MAPF ? src4[66] : 0.f;
+        o.w = f + 3 < RL::MAPF ? src4[99] : 0.f;
+        *reinterpret_cast<float4*>(maps + (((long long)J * NW + sep) * NLl + blockIdx.x * 32 + ln) * RL::MAPP + f) = o;
+    }
 }
 
 template <int R, int C>
 __host__ inline size_t ka_smem(int NWA) {
     using RL = Rec<R, C>;
-    return ((size_t)RL::REC * (NWA * 32 + 1) + (size_t)(NWA > 1 ? NWA - 1 : 1) * R * RL::RSM * 32) * sizeof(float);
+    // records (reused for the map staging area), then the back-substitution rows
+    const size_t recs = (size_t)RL::REC * (NWA * 32 + 1), stage = (size_t)(NWA > 1 ? NWA - 1 : 1) * RL::MAPP * 33;
+    return ((recs > stage ? recs : stage) + (size_t)(NWA > 1 ? NWA - 1 : 1) * R * RL::RSM * 32) * sizeof(float);
 }
 
 // Interior solve of one chunk with both separators known (zl: previous
@@ -1374,6 +1411,7 @@ struct TileOut {
     int nwa;        // chunks per KA tile (the tiles KA's separator maps refer to)
     int psa;        // KA tiles per band
     int early;      // the predecessor is a K2 launch (it waited for KA): KA's maps may be read before the wait
+    int nwa_shift;  // log2(nwa) when nwa is a power of two, else -1
     // interpolate_sparse's last pass (proj/src/smoother.cpp:149-161): channel C-1
     // is the smoothed mask d; out gets C-1 channels num/d (0 where d < floor)
     // and und[pixel] = (d < floor), instead of the C smoothed channels
@@ -1537,26 +1575,31 @@ __host__ inline size_t k2_slab_solve_smem(int NG) {
 // (a map of the tile's zA = zsep[JA-1], zB = zsep[JA]) or zB itself; its left
 // separator sigma_{j-1} is inner in the same tile (s > 0) or zA -- so the two
 // super-separators zA, zB are all a chunk reads from K2.
-__device__ __forceinline__ bool inner_separator(const PassGeom& g, const TileOut& to, int js) {
-    if (js < 0) return false;
-    const int JA = js / to.nwa;
-    return js - JA * to.nwa < to.nwa - 1 && js < g.P - 1;
-}
-
-// x = a + B zA + Cm zB from a map staged in shared memory (fields at ms[f*32])
+// x = a + B zA + Cm zB from a lane's map staged in shared memory (MAPP
+// contiguous floats, read as float4: a 48-byte lane stride is conflict-free)
 template <int R, int C>
 __device__ __forceinline__ void apply_map(const float* ms, const float (&zA)[R][C], const float (&zB)[R][C],
                                           float (&z)[R][C]) {
-    constexpr int NB = Rec<R, C>::NB;
+    using RL = Rec<R, C>;
+    constexpr int NB = RL::NB;
+    float m[RL::MAPP];
+#pragma unroll
+    for (int f = 0; f < RL::MAPP; f += 4) {
+        const float4 v = *reinterpret_cast<const float4*>(ms + f);
+        m[f] = v.x;
+        m[f + 1] = v.y;
+        m[f + 2] = v.z;
+        m[f + 3] = v.w;
+    }
 #pragma unroll
     for (int q = 0; q < R; ++q)
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            float v = ms[(q * NB + c) * 32];
+            float v = m[q * NB + c];
 #pragma unroll
-            for (int p = 0; p < R; ++p) v = fmaf(ms[(q * NB + C + p) * 32], zA[p][c], v);
+            for (int p = 0; p < R; ++p) v = fmaf(m[q * NB + C + p], zA[p][c], v);
 #pragma unroll
-            for (int p = 0; p < R; ++p) v = fmaf(ms[(q * NB + C + R + p) * 32], zB[p][c], v);
+            for (int p = 0; p < R; ++p) v = fmaf(m[q * NB + C + R + p], zB[p][c], v);
             z[q][c] = v;
         }
 }
@@ -1656,22 +1699,24 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     // this chunk's separator maps -> shared memory (per warp: slot 0 = sigma_{j-1},
     // slot 1 = sigma_j), asynchronously; before the wait when KA is not the predecessor
     using RL = Rec<R, C>;
-    float* mapsm = inv_col + ((ncol + 3) & ~3) + wid * 2 * RL::MAPF * 32 + lane;
-    const int JA = j / to.nwa, sj = j - JA * to.nwa;
+    // per warp: [slot][lane][MAPP], 16-byte aligned
+    float* mapsm = inv_col + ((ncol + 3) & ~3) + (wid * 2 * 32 + lane) * RL::MAPP;
+    const int JA = to.nwa_shift >= 0 ? j >> to.nwa_shift : j / to.nwa, sj = j - JA * to.nwa;
     const bool lastc = (j == g.P - 1) && !g.has_next;
     const bool has_left = j > 0 || g.has_prev;
-    const bool r_inner = !lastc && inner_separator(g, to, j);
+    const bool r_inner = !lastc && sj < to.nwa - 1 && j < g.P - 1;  // sigma_j inner in KA tile JA
     const bool l_inner = sj > 0;  // sigma_{j-1} inner in the same KA tile
     auto fetch_maps = [&]() {
         if (!(active && multi)) return;
-        const float* gp = maps + (long long)j * RL::MAPF * NLl + L;
+        const float* gp = maps + ((long long)j * NLl + L) * RL::MAPP;
         if (l_inner) {
+            const float* gl = gp - NLl * RL::MAPP;
 #pragma unroll
-            for (int f = 0; f < RL::MAPF; ++f) cp_async4(mapsm + f * 32, gp - (RL::MAPF - f) * NLl);
+            for (int f = 0; f < RL::MAPP; f += 4) cp_async16(mapsm + f, gl + f);
         }
         if (r_inner) {
 #pragma unroll
-            for (int f = 0; f < RL::MAPF; ++f) cp_async4(mapsm + (RL::MAPF + f) * 32, gp + f * NLl);
+            for (int f = 0; f < RL::MAPP; f += 4) cp_async16(mapsm + 32 * RL::MAPP + f, gp + f);
         }
         cp_async_commit();
     };
@@ -1742,7 +1787,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             }
         cp_async_wait_all();  // this lane's own map columns (no cross-lane reads: no warp barrier)
         if (r_inner) {
-            apply_map<R, C>(mapsm + RL::MAPF * 32, zA, zB, zr);
+            apply_map<R, C>(mapsm + 32 * RL::MAPP, zA, zB, zr);
         } else if (!lastc) {
 #pragma unroll
             for (int q = 0; q < R; ++q)
@@ -1954,7 +1999,7 @@ template <int R, int C>
 __host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
     const int n4 = (TR * C + 3) & ~3;
     const size_t tile = (size_t)ncol * (n4 + (n4 % 8 == 0 ? 4 : 8));
-    return (((tile + 3) & ~(size_t)3) + ((ncol + 3) & ~3) + (size_t)NW * 2 * Rec<R, C>::MAPF * 32) * sizeof(float);
+    return (((tile + 3) & ~(size_t)3) + ((ncol + 3) & ~3) + (size_t)NW * 2 * Rec<R, C>::MAPP * 32) * sizeof(float);
 }
 
 
@@ -2029,8 +2074,9 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
         // triggering) or, with a single KA tile per band, KA itself
         const bool early = slab || PSA > 1;
-        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, pl.ratio, pl.ratio_floor,
-                   pl.und};
+        const int nwa_shift = (NWA & (NWA - 1)) == 0 ? __builtin_ctz((unsigned)NWA) : -1;
+        TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, nwa_shift, pl.ratio,
+                   pl.ratio_floor, pl.und};
         const dim3 kgrid(pl.ncta, PB, g.batch);
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
