@@ -18,7 +18,7 @@ can also be timed with --config.
 * e2e        -- same metric through the public host-pointer C ABI
                 (sgwls_b200_smooth / _interpolate_sparse_batch) from pinned host
                 buffers: H2D of the inputs and D2H of the result every step.
-* roofline   -- one pass (K1..K4) as the unit: algorithmic bytes of a pass
+* roofline   -- one pass (KA, K2, KB) as the unit: algorithmic bytes of a pass
                 (4*M*N*(2C+G) per image) / mean pass duration,
                 measured live with the library's per-launch CUDA events;
                 peak = MEASURED_PEAKS.json hbm_gbs.
@@ -343,9 +343,10 @@ def main():
     roofline = {
         "bound": "hbm", "unit": "GB/s", "peak": peak, "peak_source": peak_src,
         "achieved": achieved, "frac": achieved / peak, "traffic": traffic,
-        "launch_unit": "one directional pass: ka_tile (chunk spike-forward + in-tile reduction; solves the "
-                       "reduced system itself when short) [+ k2_tree (super-separator solve)] + kb_tile (interior "
-                       "solve + averaging + transposed store); duration = timed step / T"
+        "launch_unit": "one directional pass: ka_tile (chunk spike-forward, in-tile reduction -> super-record, "
+                       "affine maps of the tile's inner separators) [+ k2_tree (super-separators)] + kb_tile "
+                       "(separators from the maps, interior solve, averaging, transposed store); duration = timed "
+                       "step / T"
                        + (("; sharded: includes the slab-record all-gather and halo exchange"
                            if args.shard_mode == "slabs" else "; sharded: includes the all-to-all transpose")
                           if sharded else ""),
@@ -363,6 +364,8 @@ def main():
         launches = sm.kernel_launches()
     else:
         launches = S.kernel_launches(wl.width, wl.height, wl.channels, 1, batch_per_rank, wl.sparse, cfg)
+        if wl.sparse:
+            launches += 1  # the field validation kernel (validate=True)
 
     # ---- e2e through the host-pointer C ABI from pinned buffers
     e2e = None

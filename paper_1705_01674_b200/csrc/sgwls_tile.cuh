@@ -989,7 +989,7 @@ __device__ __forceinline__ void solve_inner(const float* recs, long long rs, lon
 template <int R, int C>
 __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec,
                                              float* __restrict__ rsc, float* __restrict__ z, float* sm, int lane,
-                                             int w, int NG, int group) {
+                                             int w, int NG, int group, bool staged) {
     using RL = Rec<R, C>;
     const int NL = g.nb * g.batch;
     const int L = group * 32 + lane;
@@ -1003,9 +1003,29 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     float* grec = sm;
     float* zg = grec + RL::REC * rsG;
     float* bsg = zg + NG * R * C * 32;
-    const float* my = rec + (long long)J0 * RL::REC * NLl + L;
-    if (w < NGa && ok)
-        reduce_super<R, C, (R >= SGWLS_REC_PF_MINR)>(my, NLl, (long long)RL::REC * NLl, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
+    // staged (short reduced systems, c1/c2): the CTA first copies all its lines'
+    // super-records into shared memory with every thread (one latency), and the
+    // level-3 back-substitution rows stay there too -- levels 1 and 3 then run
+    // from shared memory instead of waiting an L2 round trip per record
+    float* srs = bsg + NG * R * RL::RSM * 32;  // [J][field][lane]
+    float* sbs = srs + PSn * RL::REC * 32;     // [J][R][RS][lane]
+    if (staged) {
+        const int tot = PSn * RL::REC * 32, NT = NG * 32, tid = w * 32 + lane;
+        for (int i = tid; i < tot; i += NT) {
+            const int row = i >> 5, Lg = group * 32 + (i & 31);
+            srs[i] = Lg < NL ? __ldcg(rec + (long long)row * NLl + Lg) : 0.f;
+        }
+        __syncthreads();
+    }
+    const float* my = staged ? srs + J0 * RL::REC * 32 + lane : rec + (long long)J0 * RL::REC * NLl + L;
+    const long long fst = staged ? 32 : NLl;  // field stride of `my`
+    if (w < NGa && ok) {
+        if (staged)
+            reduce_super<R, C, false>(my, fst, RL::REC * fst, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
+        else
+            reduce_super<R, C, (R >= SGWLS_REC_PF_MINR)>(my, fst, RL::REC * fst, gsz, w == 0, w == NGa - 1,
+                                                         grec + w * 32 + lane, rsG);
+    }
     __syncthreads();
     // level 2 as a binary tree over the NGa group records: pairwise merges up
     // (segment [a, a+span) absorbs [a+span, a+2span), eliminating group
@@ -1059,25 +1079,32 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-        solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(my, NLl, (long long)RL::REC * NLl, gsz, has_l, zL, has_r, zR,
-                          z + (long long)J0 * R * C * NLl + L, NLl, rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
+        if (staged)
+            solve_inner<R, C, false>(my, fst, RL::REC * fst, gsz, has_l, zL, has_r, zR,
+                                     z + (long long)J0 * R * C * NLl + L, NLl, sbs + J0 * R * RL::RS * 32 + lane, 32);
+        else
+            solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(my, fst, RL::REC * fst, gsz, has_l, zL, has_r, zR,
+                                                        z + (long long)J0 * R * C * NLl + L, NLl,
+                                                        rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
     }
 }
 
 // MAXT: 512 threads (<= 128 registers) up to 16 groups; 1024 (<= 64) for 32
 template <int R, int C, int MAXT>
 __global__ void __launch_bounds__(MAXT) k2_tree(const PassGeom g, const float* __restrict__ rec,
-                                               float* __restrict__ rsc, float* __restrict__ z) {
+                                               float* __restrict__ rsc, float* __restrict__ z, int staged) {
     extern __shared__ float sm[];
     pdl_wait();     // KA's records
     pdl_trigger();  // KB may launch now: everything it reads before its own wait (KA's output) is complete
-    k2_tree_body<R, C>(g, rec, rsc, z, sm, threadIdx.x, threadIdx.y, blockDim.y, blockIdx.x);
+    k2_tree_body<R, C>(g, rec, rsc, z, sm, threadIdx.x, threadIdx.y, blockDim.y, blockIdx.x, staged != 0);
 }
 
 template <int R, int C>
-__host__ inline size_t k2_tree_smem(int NG) {
+__host__ inline size_t k2_tree_smem(int NG, int PS = 0) {
     using RL = Rec<R, C>;
-    return ((size_t)RL::REC * (NG * 32 + 1) + (size_t)NG * R * C * 32 + (size_t)NG * R * RL::RSM * 32) * sizeof(float);
+    return ((size_t)RL::REC * (NG * 32 + 1) + (size_t)NG * R * C * 32 + (size_t)NG * R * RL::RSM * 32 +
+            (size_t)PS * (RL::REC + R * RL::RS) * 32) *
+           sizeof(float);
 }
 
 // ===================================================================== KA
@@ -1155,10 +1182,14 @@ __device__ __forceinline__ void ka_chunk(const PassGeom& g, const float* __restr
 template <int R, int C, int CG>
 __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, float* __restrict__ srec,
-                                               float* __restrict__ maps, const __grid_constant__ WeightDev W) {
+                                               float* __restrict__ maps, const __grid_constant__ WeightDev W, int NW) {
     using RL = Rec<R, C>;
     extern __shared__ float sm[];
-    const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
+    // NW chunks per tile, NWK (= blockDim.y <= NW) warps: each warp runs
+    // chunks wid, wid + NWK, ...  Fewer warps than chunks shrink the share of
+    // warps idling while warp 0 reduces the tile (with one warp per chunk, ncu
+    // measured 43 % of KA's warp time at that barrier on c5)
+    const int lane = threadIdx.x, wid = threadIdx.y, NWK = blockDim.y;
     const int NL = g.nb * g.batch;
     // grid: (line group, tile)
     const int L = blockIdx.x * 32 + lane;
@@ -1167,7 +1198,8 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     const int rs = NW * 32 + 1;  // smem record field stride
     pdl_wait();  // the pass input is the previous pass's output
     pdl_trigger();
-    if (L < NL && wid < nw) ka_chunk<R, C, CG>(g, src, guid, W, L, J * NW + wid, sm + wid * 32 + lane, rs);
+    if (L < NL)
+        for (int c = wid; c < nw; c += NWK) ka_chunk<R, C, CG>(g, src, guid, W, L, J * NW + c, sm + c * 32 + lane, rs);
     __syncthreads();
     const int PS = gridDim.y;  // = ceil(P / NW), the grid's tile dimension
     const long long NLl = NL;
@@ -1183,14 +1215,14 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     // per warp, staged in shared memory (the record area is free by now) ...
     float* mst = sm + lane;
     if (L < NL)
-        for (int b = wid; b < RL::NB; b += NW) maps_backward_column<R, C>(bsm, nw, last_super, b, mst);
+        for (int b = wid; b < RL::NB; b += NWK) maps_backward_column<R, C>(bsm, nw, last_super, b, mst);
     __syncthreads();
     // ... and written out as whole 16-byte vectors: a separator's maps for the
     // tile's 32 lines are one contiguous run of 32*MAPP floats ([chunk][line][MAPP])
     constexpr int V = RL::MAPP / 4;  // float4 per line
     const int nv = (nw - 1) * 32 * V;
     const int ngl = min(32, NL - (int)blockIdx.x * 32);  // lines of this group
-    for (int v = wid * 32 + lane; v < nv; v += NW * 32) {
+    for (int v = wid * 32 + lane; v < nv; v += NWK * 32) {
         const int sep = v / (32 * V), rem = v - sep * 32 * V, ln = rem / V, f = (rem - ln * V) * 4;
         if (ln >= ngl) continue;
         const float* src4 = sm + (sep * RL::MAPP + f) * 33 + ln;
@@ -2022,8 +2054,32 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         const size_t smem = ka_smem<R, C>(NWA);
         e = cudaFuncSetAttribute(ka_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, NWA), smem, st, g, pl.src, pl.guid,
-                       pl.rec, pl.maps, *pl.w);
+        // warps per KA CTA: NWA (one chunk each), or NWA/2 (two chunks each)
+        // when that keeps as many warps resident per SM and the grid is several
+        // waves deep -- fewer warps idle while warp 0 reduces the tile (c5: 4
+        // warps x 2 chunks, KA -15 %; c4 / c3 / r = 1 keep one chunk per warp)
+        static const int kaw_env = [] {
+            const char* v = std::getenv("SGWLS_KA_CTA_WARPS");  // schedule knob: warps per KA CTA
+            return v ? std::atoi(v) : 0;
+        }();
+        int kaw = NWA;
+        if (kaw_env > 0) {
+            kaw = kaw_env < NWA ? kaw_env : NWA;
+        } else if (NWA % 2 == 0) {
+            static int nsm = 0;
+            if (!nsm) {
+                int dev = 0;
+                cudaGetDevice(&dev);
+                cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+            }
+            int occ_full = 0, occ_half = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_full, ka_tile<R, C, CG>, 32 * NWA, smem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_half, ka_tile<R, C, CG>, 16 * NWA, smem);
+            const long long warps = (long long)((NL + 31) / 32) * PSA * NWA;
+            if (occ_half * (NWA / 2) >= occ_full * NWA && warps >= 4LL * nsm * occ_full * NWA) kaw = NWA / 2;
+        }
+        e = launch_pdl(ka_tile<R, C, CG>, dim3((NL + 31) / 32, PSA), dim3(32, kaw), smem, st, g, pl.src, pl.guid,
+                       pl.rec, pl.maps, *pl.w, NWA);
         if (e != cudaSuccess) return e;
     }
     if (pl.slab_phase == 1) {  // row-slab phase A: this slab's record
@@ -2059,11 +2115,16 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         int NG = ng_env ? ng_env : (PSA >= 128 && R <= 2 ? 32 : (PSA >= 20 ? 16 : 8));
         if (R > 2 && NG > 16) NG = 16;  // 1024 threads hold only 64 registers
         while (NG > 4 && k2_tree_smem<R, C>(NG) > 200 * 1024) NG /= 2;
-        const size_t sm2 = k2_tree_smem<R, C>(NG);
+        // staging all the CTA's super-records in shared memory first (one latency)
+        // was measured slower on the short systems of c1 / c2 (their groups hold
+        // only 2-3 records): off; kept as an option of the kernel
+        const bool staged = false;
+        const size_t sm2 = k2_tree_smem<R, C>(NG, staged ? PSA : 0);
         auto kern = NG > 16 ? k2_tree<R, C, 1024> : k2_tree<R, C, 512>;
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm2);
         if (e != cudaSuccess) return e;
-        e = launch_pdl(kern, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs, pl.z);
+        e = launch_pdl(kern, dim3((NL + 31) / 32), dim3(32, NG), sm2, st, gs, (const float*)pl.rec, pl.rs, pl.z,
+                       staged ? 1 : 0);
         if (e != cudaSuccess) return e;
     }
     {
