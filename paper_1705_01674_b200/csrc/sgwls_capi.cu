@@ -247,7 +247,8 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         ap.nph = nph;
         ap.rec_n = P > 1 ? (size_t)PS * rec_floats(r, C) * NL : 0;
         ap.map_n = P > 1 ? (size_t)P * map_floats(r, C) * NL : 0;
-        ap.rs_n = PS > 1 ? (size_t)(PS - 1) * r * rs_floats(r, C) * NL : 0;
+        // K2 back-substitution rows with their spike column (level 1 keeps them for level 3)
+        ap.rs_n = PS > 1 ? (size_t)PS * r * (rs_floats(r, C) + r) * NL : 0;
         ap.z_n = PS > 1 ? (size_t)(PS - 1) * r * C * NL : 0;
         ap.u_n = 0;
         return ap;
@@ -685,7 +686,7 @@ SlabLayout slab_layout(int width, int rows, int C, int Cg, const sgwls_b200_conf
     };
     L.maps = take(P * map_floats(cfg->r, C) * NL);
     L.srec = take(PS * REC * NL);
-    L.rsc = take((PS > 1 ? PS - 1 : 1) * r * RS * NL);
+    L.rsc = take((PS > 1 ? PS : 1) * r * (RS + r) * NL);
     L.zext = take((PS + 1) * r * C * NL);
     L.zg = take(G * r * C * NL);
     L.bsg = take(G * r * RS * NL);

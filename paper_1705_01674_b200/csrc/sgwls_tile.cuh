@@ -778,13 +778,17 @@ __device__ __forceinline__ void reduce_super(const float* recs, long long rs, lo
 // (b: value | zL | zR basis).  Once K2 has solved the super-separators, any
 // chunk separator is 2R^2 + R FMAs away -- no third solve over the chunk
 // records (the former KC launch) and no record round trip through HBM.
-template <int R, int C>
+template <int R, int C, bool GPF = false>
 __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int nw, bool first_super,
                                                  bool last_super, float* out, long long os, float* bsm,
-                                                 int cs = 32) {
+                                                 int cs = 32, int bst = 32) {
+    // bst: stride of the back-substitution rows' fields (32 in shared memory,
+    // the line count in global scratch); GPF: recs is global, L1-prefetch ahead
     using RL = Rec<R, C>;
     constexpr int RSM = RL::RSM;
-    auto bsrow = [&](int s, int mm) { return bsm + (s * R + mm) * RSM * 32; };
+    auto bsrow = [&](int s, int mm) { return bsm + (long long)(s * R + mm) * RSM * bst; };
+    if (GPF && SGWLS_REC_PF > 0)
+        for (int s = 0; s < min(nw, SGWLS_REC_PF); ++s) prefetch_record<R, C>(recs, rs, cs, s);
     BWin<R, C, true> w;
     w.clear_all();
     if (!first_super) {
@@ -799,12 +803,13 @@ __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int 
     }
     const int nblk = last_super ? nw - 1 : nw;
     for (int s = 0; s < nblk; ++s) {
-        const float* t = recs + s * cs;
-        const float* h = recs + (s + 1) * cs;
+        if (GPF && SGWLS_REC_PF > 0 && s + SGWLS_REC_PF < nw) prefetch_record<R, C>(recs, rs, cs, s + SGWLS_REC_PF);
+        const float* t = recs + (long long)s * cs;
+        const float* h = recs + (long long)(s + 1) * cs;
         enter_block<R, C, true>(w, t, h, rs, s < nw - 1, s > 0, s > 0 || !first_super);
         if (s > 0) {
 #pragma unroll
-            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, bsrow(s - 1, mm), 32);
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, bsrow(s - 1, mm), bst);
         }
         w.shift();
     }
@@ -812,7 +817,7 @@ __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int 
         if (nblk > 0) {
             w.clear_hi();
 #pragma unroll
-            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, bsrow(nblk - 1, mm), 32);
+            for (int mm = 0; mm < R; ++mm) w.elim(0, mm, !first_super, bsrow(nblk - 1, mm), bst);
         }
     } else {
 #pragma unroll
@@ -843,19 +848,19 @@ __device__ __forceinline__ void reduce_super_fwd(const float* recs, int rs, int 
 // separators either side: zL (spike side) and zR (the window's hi block).
 template <int R, int C>
 __device__ __forceinline__ void solve_from_bs(const float* bs, const float (&zL)[R][C], const float (&zR)[R][C],
-                                              float (&x)[R][C]) {
+                                              float (&x)[R][C], long long bst = 32) {
     constexpr int RSM = Rec<R, C>::RSM;
 #pragma unroll
     for (int mm = R - 1; mm >= 0; --mm) {
-        const float* o = bs + mm * RSM * 32;
+        const float* o = bs + mm * RSM * bst;
 #pragma unroll
         for (int c = 0; c < C; ++c) {
-            float v = o[(2 * R - 1 + c) * 32];
+            float v = o[(2 * R - 1 + c) * bst];
 #pragma unroll
             for (int i = mm + 1; i < 2 * R; ++i)
-                v = fmaf(o[(i - mm - 1) * 32], (i < R) ? x[i < R ? i : 0][c] : zR[i >= R ? i - R : 0][c], v);
+                v = fmaf(o[(i - mm - 1) * bst], (i < R) ? x[i < R ? i : 0][c] : zR[i >= R ? i - R : 0][c], v);
 #pragma unroll
-            for (int q = 0; q < R; ++q) v = fmaf(o[(2 * R - 1 + C + q) * 32], zL[q][c], v);
+            for (int q = 0; q < R; ++q) v = fmaf(o[(2 * R - 1 + C + q) * bst], zL[q][c], v);
             x[mm][c] = v;
         }
     }
@@ -1019,12 +1024,16 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
     }
     const float* my = staged ? srs + J0 * RL::REC * 32 + lane : rec + (long long)J0 * RL::REC * NLl + L;
     const long long fst = staged ? 32 : NLl;  // field stride of `my`
+    // level 1 keeps its back-substitution rows (global scratch, [J][R][RSM][line]),
+    // so level 3 is a backward sweep only
+    float* bs1 = rsc + (long long)J0 * R * RL::RSM * NLl + L;
     if (w < NGa && ok) {
         if (staged)
             reduce_super<R, C, false>(my, fst, RL::REC * fst, gsz, w == 0, w == NGa - 1, grec + w * 32 + lane, rsG);
         else
-            reduce_super<R, C, (R >= SGWLS_REC_PF_MINR)>(my, fst, RL::REC * fst, gsz, w == 0, w == NGa - 1,
-                                                         grec + w * 32 + lane, rsG);
+            reduce_super_fwd<R, C, (R >= SGWLS_REC_PF_MINR)>(my, (int)fst, gsz, w == 0, w == NGa - 1,
+                                                             grec + w * 32 + lane, rsG, bs1, RL::REC * (int)fst,
+                                                             (int)NLl);
     }
     __syncthreads();
     // level 2 as a binary tree over the NGa group records: pairwise merges up
@@ -1079,13 +1088,35 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
 #pragma unroll
                 for (int c = 0; c < C; ++c) zo[(q * C + c) * NLl] = zR[q][c];
         }
-        if (staged)
+        if (staged) {
             solve_inner<R, C, false>(my, fst, RL::REC * fst, gsz, has_l, zL, has_r, zR,
                                      z + (long long)J0 * R * C * NLl + L, NLl, sbs + J0 * R * RL::RS * 32 + lane, 32);
-        else
-            solve_inner<R, C, (R >= SGWLS_REC_PF_MINR)>(my, fst, RL::REC * fst, gsz, has_l, zL, has_r, zR,
-                                                        z + (long long)J0 * R * C * NLl + L, NLl,
-                                                        rsc + (long long)J0 * R * RL::RS * NLl + L, NLl);
+        } else {
+            // backward sweep over level 1's rows: x_s from x_{s+1} (zR for the last) and zL
+            float xn[R][C];
+#pragma unroll
+            for (int q = 0; q < R; ++q)
+#pragma unroll
+                for (int c = 0; c < C; ++c) xn[q][c] = zR[q][c];
+            for (int sep = gsz - 2; sep >= 0; --sep) {
+                const float* o = bs1 + (long long)sep * R * RL::RSM * NLl;
+                if (sep > 0) {  // L1-prefetch the next rows of the chain
+#pragma unroll
+                    for (int f = 0; f < R * RL::RSM; ++f)
+                        asm volatile("prefetch.global.L1 [%0];" ::"l"(o - (long long)(R * RL::RSM - f) * NLl));
+                }
+                float x[R][C];
+                solve_from_bs<R, C>(o, zL, xn, x, NLl);
+                float* zo = z + (long long)(J0 + sep) * R * C * NLl + L;
+#pragma unroll
+                for (int q = 0; q < R; ++q)
+#pragma unroll
+                    for (int c = 0; c < C; ++c) {
+                        zo[(q * C + c) * NLl] = x[q][c];
+                        xn[q][c] = x[q][c];
+                    }
+            }
+        }
     }
 }
 
