@@ -139,8 +139,6 @@ int sgwls_b200_profile_read(char* json, size_t len);
  * call after every replay when profiling graph-replayed calls. */
 void sgwls_b200_profile_collect(void);
 
-/* Library version string. */
-
 /* ---- row-slab mode: one Column pass of an image split into row slabs ----
  * (one slab per GPU; paper_1705_01674_b200/sharded.py).  The
  * band solves are partitioned exactly across slabs: phase A computes each
@@ -227,7 +225,21 @@ int sgwls_b200_colorize(const float* gray, int gray_channels, const float* scrib
                         const float* scribble_mask, int width, int height, const sgwls_b200_config* cfg, float* out,
                         char* err, size_t errlen);
 
+/* Library version string. */
 const char* sgwls_b200_version(void);
+
+/* ---- image files (proj/include/sgwls/image.hpp:38-46, proj/src/image.cpp:111-250) ----
+ * read_image: PGM (P2/P5), PPM (P3/P6) scaled to [0,1] (maxval <= 255 -> /255, else /65535,
+ * 16-bit samples big-endian) and PFM (Pf/PF, raw floats, bottom-up rows, the scale's sign
+ * is the byte order).  *data is malloc'ed (release with sgwls_b200_image_free), row-major
+ * channel-interleaved.  write_image: by extension .pgm (P5, 1 channel), .ppm (P6, 3
+ * channels), .pfm; LDR writers clamp to [0,1] and quantise round-half-up to 255.
+ * Failures return SGWLS_B200_EINVAL with the reference's text ("<path>: byte N: ..."). */
+int sgwls_b200_image_read(const char* path, float** data, int* width, int* height, int* channels, char* err,
+                          size_t errlen);
+void sgwls_b200_image_free(float* data);
+int sgwls_b200_image_write(const char* path, const float* data, int width, int height, int channels, char* err,
+                           size_t errlen);
 
 /* CUDA-graph cache of SGWLS_B200_GRAPH calls: an LRU of at most 64 entries per
  * process.  _clear waits for and releases every cached graph (returns how many

@@ -232,3 +232,44 @@ class RefApps:
         self._call(self.lib.ref_colorize_f32, g.ctypes.data, s.ctypes.data, m.ctypes.data, w, h,
                    C.byref(make_config(cfg)), out.ctypes.data)
         return out
+
+
+class RefImageIO:
+    """The reference's image codecs (proj/src/image.cpp:194-250) through
+    oracle/_ref/ref_imgtool (its own process, see oracle/ref_imgtool.cpp): the checker
+    of paper_1705_01674_b200.read_image / write_image and of the CLI's files."""
+
+    TOOL = os.path.join(HERE, "_ref", "ref_imgtool")
+
+    def __init__(self):
+        if not os.path.exists(self.TOOL) and os.path.isdir("/root/reference/proj/src"):
+            build(ref=True)
+        if not os.path.exists(self.TOOL):
+            raise FileNotFoundError(self.TOOL)
+
+    def _run(self, *args) -> str:
+        import subprocess
+        r = subprocess.run([self.TOOL, *map(str, args)], capture_output=True, text=True)
+        if r.returncode == 1:
+            raise OracleError(r.stderr.strip())
+        if r.returncode != 0:
+            raise RuntimeError(f"ref_imgtool rc={r.returncode}: {r.stderr}")
+        return r.stdout
+
+    def read(self, path: str) -> np.ndarray:
+        import tempfile
+        with tempfile.TemporaryDirectory() as d:
+            raw = os.path.join(d, "img.f64")
+            w, h, c = map(int, self._run("read", path, raw).split())
+            return np.fromfile(raw, dtype=np.float64).reshape(h, w, c)
+
+    def write(self, img: np.ndarray, path: str) -> None:
+        import tempfile
+        a = np.ascontiguousarray(img, dtype=np.float64)
+        if a.ndim == 2:
+            a = a[:, :, None]
+        h, w, c = a.shape if a.size else (0, 0, 1)
+        with tempfile.TemporaryDirectory() as d:
+            raw = os.path.join(d, "img.f64")
+            a.tofile(raw)
+            self._run("write", raw, w, h, c, path)

@@ -19,6 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libsgwls_b200.so")
 INCLUDE = os.path.join(ROOT, "include")
+CLI = os.path.join(PKG, "bin", "sgwls_b200")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
@@ -70,9 +71,26 @@ def build_native(verbose: bool = False, extra: list[str] | None = None, variant:
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
+    if variant is None:
+        build_cli()
     if verbose:
         print("built", lib)
     return lib
+
+
+def build_cli() -> str:
+    """The command-line tool (csrc/tools/sgwls_b200_main.cpp, the drop-in for the
+    reference's proj/tools/sgwls_main.cpp): plain C++ on the C ABI, linked against
+    the in-tree library with an $ORIGIN-relative rpath."""
+    src = os.path.join(CSRC, "tools", "sgwls_b200_main.cpp")
+    if _stale(CLI, [src, LIB, os.path.join(INCLUDE, "sgwls_b200.h")]):
+        os.makedirs(os.path.dirname(CLI), exist_ok=True)
+        cmd = ["g++", "-O2", "-std=c++17", "-Wall", "-Wextra", "-I" + INCLUDE, src, "-o", CLI, "-L" + PKG,
+               "-lsgwls_b200", "-Wl,-rpath,$ORIGIN/.."]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"g++ failed for {src}:\n{r.stdout}\n{r.stderr}")
+    return CLI
 
 
 if __name__ == "__main__":

@@ -110,6 +110,11 @@ SIGNATURES = {
     "sgwls_b200_interpolate_sparse_batch_multi": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                                             C.POINTER(NativeConfig), _P, C.c_int, _P, _P, C.c_char_p,
                                                             C.c_size_t]),
+    # image files (proj/src/image.cpp:111-250)
+    "sgwls_b200_image_read": (C.c_int, [C.c_char_p, C.POINTER(C.POINTER(C.c_float)), C.POINTER(C.c_int),
+                                        C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_char_p, C.c_size_t]),
+    "sgwls_b200_image_free": (None, [C.POINTER(C.c_float)]),
+    "sgwls_b200_image_write": (C.c_int, [C.c_char_p, _P, C.c_int, C.c_int, C.c_int, C.c_char_p, C.c_size_t]),
     # application pipelines (proj/src/apps.cpp)
     "sgwls_b200_enhance_preset": (None, [C.POINTER(NativeConfig)]),
     "sgwls_b200_tonemap_layer_preset": (None, [C.c_double, C.POINTER(NativeConfig)]),

@@ -330,3 +330,30 @@ def graph_count() -> int:
 
 def version() -> str:
     return N.lib().sgwls_b200_version().decode()
+
+
+def read_image(path: str) -> np.ndarray:
+    """sgwls::read_image (proj/include/sgwls/image.hpp:41): PGM/PPM scaled to [0,1] or PFM,
+    as an (H, W, C) float32 array; decode failures carry the reference's byte-offset text."""
+    data = C.POINTER(C.c_float)()
+    w, h, c = C.c_int(), C.c_int(), C.c_int()
+    err = N.errbuf()
+    N.check(N.lib().sgwls_b200_image_read(str(path).encode(), C.byref(data), C.byref(w), C.byref(h), C.byref(c),
+                                          err, len(err)), err)
+    try:
+        return np.ctypeslib.as_array(data, shape=(h.value, w.value, c.value)).copy()
+    finally:
+        N.lib().sgwls_b200_image_free(data)
+
+
+def write_image(img, path: str) -> None:
+    """sgwls::write_image (proj/include/sgwls/image.hpp:46): .pgm / .ppm (clamped, 8-bit,
+    round half up) or .pfm by extension."""
+    a = np.asarray(img, dtype=np.float32)
+    if a.ndim == 2:
+        a = a[:, :, None]
+    a = np.ascontiguousarray(a)
+    err = N.errbuf()
+    ptr = a.ctypes.data_as(C.c_void_p) if a.size else None
+    h, w, c = (a.shape if a.ndim == 3 else (0, 0, 0))
+    N.check(N.lib().sgwls_b200_image_write(str(path).encode(), ptr, w, h, c, err, len(err)), err)
