@@ -116,26 +116,63 @@ __global__ void k_ratio(const float* __restrict__ packed, float* __restrict__ ou
 // Sparse-field validation (proj/src/smoother.cpp:129-144).  status[0] = min
 // violating pixel index (mask not 0/1, or value nonzero where mask is 0),
 // status[1] = number of pixels with mask == 1 (saturating).
-__global__ void k_validate_sparse(const float* __restrict__ values, const float* __restrict__ mask, long long npx,
-                                  int C, int batch, unsigned long long* status) {
-    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+// One pixel's field checks (proj/src/smoother.cpp:133-141): mask in {0, 1}, values zero outside it
+__device__ __forceinline__ void check_px(float mv, bool vnz, long long i, bool& any, long long& bad) {
+    if ((mv != 0.f && mv != 1.f) || (mv == 0.f && vnz)) bad = bad < i ? bad : i;
+    any = any || mv == 1.f;
+}
+
+// Streams mask and values once: VPT pixels per thread and step as 16-byte loads when the
+// layout allows (all loads of a step issued before any test), one atomic per CTA at most.
+// status[pair] = first offending pixel (row-major, min), status[batch + pair] = mask non-empty.
+template <int C>
+__global__ void __launch_bounds__(256) k_validate_sparse(const float* __restrict__ values,
+                                                        const float* __restrict__ mask, long long npx, int Crt,
+                                                        int batch, unsigned long long* status, int vec) {
     const int bi = blockIdx.y;  // pair
-    values += (long long)bi * npx * C;
+    const int Cn = C > 0 ? C : Crt;
+    values += (long long)bi * npx * Cn;
     mask += (long long)bi * npx;
     unsigned long long* any_w = status + batch + bi;
-    status += bi;
     bool any = false;
-    if (i < npx) {
-        const float mv = mask[i];
-        bool bad = false;
-        if (mv != 0.f && mv != 1.f) bad = true;
-        if (mv == 1.f) any = true;
-        if (mv == 0.f)
-            for (int c = 0; c < C; ++c)
-                if (values[i * C + c] != 0.f) bad = true;
-        if (bad) atomicMin(&status[0], (unsigned long long)i);
+    long long bad = 0x7fffffffffffffffLL;
+    if (vec && C == 1) {
+        const long long nq = npx >> 2;
+        const float4* m4 = reinterpret_cast<const float4*>(mask);
+        const float4* v4 = reinterpret_cast<const float4*>(values);
+        constexpr int U = 4;
+        for (long long q0 = (long long)blockIdx.x * blockDim.x * U + threadIdx.x; q0 < nq;
+             q0 += (long long)gridDim.x * blockDim.x * U) {
+            float4 m[U], v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long q = q0 + (long long)u * blockDim.x;
+                m[u] = q < nq ? __ldcs(m4 + q) : make_float4(1.f, 1.f, 1.f, 1.f);
+                v[u] = q < nq ? __ldcs(v4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long q = q0 + (long long)u * blockDim.x;
+                if (q < nq) {
+                    check_px(m[u].x, v[u].x != 0.f, 4 * q, any, bad);
+                    check_px(m[u].y, v[u].y != 0.f, 4 * q + 1, any, bad);
+                    check_px(m[u].z, v[u].z != 0.f, 4 * q + 2, any, bad);
+                    check_px(m[u].w, v[u].w != 0.f, 4 * q + 3, any, bad);
+                }
+            }
+        }
+    } else {
+        for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < npx;
+             i += (long long)gridDim.x * blockDim.x) {
+            const float mv = mask[i];
+            bool vnz = false;
+            for (int c = 0; c < Cn; ++c) vnz = vnz || values[i * Cn + c] != 0.f;
+            check_px(mv, vnz, i, any, bad);
+        }
     }
-    if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(any_w, 1ull);
+    if (bad != 0x7fffffffffffffffLL) atomicMin(&status[bi], (unsigned long long)bad);
+    if (__syncthreads_or(any) && threadIdx.x == 0 && *reinterpret_cast<volatile unsigned long long*>(any_w) == 0ull)
+        atomicOr(any_w, 1ull);
 }
 
 // =========================================================== dispatch
@@ -210,8 +247,18 @@ cudaError_t launch_ratio(const float* packed, float* out, float* und, long long 
 cudaError_t launch_validate_sparse(const float* values, const float* mask, long long npx, int C, int batch,
                                    unsigned long long* status, cudaStream_t st) {
     ProfScope ps("validate_sparse", st);
-    k_validate_sparse<<<dim3((unsigned)((npx + 255) / 256), (unsigned)batch), 256, 0, st>>>(values, mask, npx, C, batch,
-                                                                                           status);
+    const bool vec = C == 1 && npx % 4 == 0 && ((reinterpret_cast<uintptr_t>(values) | reinterpret_cast<uintptr_t>(mask)) & 15) == 0;
+    // 16 pixels per thread and step on the vector path; a few CTAs per SM over the whole batch
+    const long long per_cta = vec ? 256LL * 16 : 256LL * 4;
+    long long bx = (npx + per_cta - 1) / per_cta;
+    const long long cap = (148LL * 16 + batch - 1) / batch;
+    if (bx > cap) bx = cap;
+    if (bx < 1) bx = 1;
+    const dim3 grid((unsigned)bx, (unsigned)batch);
+    if (C == 1)
+        k_validate_sparse<1><<<grid, 256, 0, st>>>(values, mask, npx, C, batch, status, vec ? 1 : 0);
+    else
+        k_validate_sparse<0><<<grid, 256, 0, st>>>(values, mask, npx, C, batch, status, 0);
     return cudaGetLastError();
 }
 

@@ -1250,19 +1250,29 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
     __syncthreads();
     // ... and written out as whole 16-byte vectors: a separator's maps for the
     // tile's 32 lines are one contiguous run of 32*MAPP floats ([chunk][line][MAPP])
-    constexpr int V = RL::MAPP / 4;  // float4 per line
-    const int nv = (nw - 1) * 32 * V;
+    // thread -> one (line, float4) slot of the tile's 32*V per separator, looping over the
+    // separators (no per-element index divisions); spare thread groups take alternate separators
+    constexpr int V = RL::MAPP / 4, PER = 32 * V;  // float4 per line, per separator
+    const int NT = NWK * 32, tid = wid * 32 + lane;
+    const int groups = NT >= PER ? NT / PER : 1;
+    const int gq = tid / PER;
     const int ngl = min(32, NL - (int)blockIdx.x * 32);  // lines of this group
-    for (int v = wid * 32 + lane; v < nv; v += NWK * 32) {
-        const int sep = v / (32 * V), rem = v - sep * 32 * V, ln = rem / V, f = (rem - ln * V) * 4;
-        if (ln >= ngl) continue;
-        const float* src4 = sm + (sep * RL::MAPP + f) * 33 + ln;
-        float4 o;
-        o.x = src4[0];
-        o.y = f + 1 < RL::MAPF ? src4[33] : 0.f;
-        o.z = f + 2 < RL::MAPF ? src4[66] : 0.f;
-        o.w = f + 3 < RL::MAPF ? src4[99] : 0.f;
-        *reinterpret_cast<float4*>(maps + (((long long)J * NW + sep) * NLl + blockIdx.x * 32 + ln) * RL::MAPP + f) = o;
+    if (gq < groups) {
+        for (int i = tid - gq * PER; i < PER; i += NT) {
+            const int ln = i / V, f = (i - ln * V) * 4;
+            if (ln >= ngl) continue;
+            const float* s4 = sm + f * 33 + ln;
+            float* dst = maps + ((long long)J * NW * NLl + blockIdx.x * 32 + ln) * RL::MAPP + f;
+            for (int sep = gq; sep < nw - 1; sep += groups) {
+                const float* src4 = s4 + sep * RL::MAPP * 33;
+                float4 o;
+                o.x = src4[0];
+                o.y = f + 1 < RL::MAPF ? src4[33] : 0.f;
+                o.z = f + 2 < RL::MAPF ? src4[66] : 0.f;
+                o.w = f + 3 < RL::MAPF ? src4[99] : 0.f;
+                *reinterpret_cast<float4*>(dst + (long long)sep * NLl * RL::MAPP) = o;
+            }
+        }
     }
 }
 
@@ -1410,10 +1420,15 @@ __device__ __forceinline__ void average_shfl(const float (&ys)[K][C], int nrw, i
 // of the shared output tile: lane l's column x = xa + TAU*l + j is output row x,
 // and this chunk's RW rows are RW*C consecutive floats of it (vector stores of
 // VEC floats; the last, short chunk stores scalars).  Only owned columns.
-template <int TAU, int R, int C, int K, int VEC>
+// INTERIOR (inv_col == nullptr is not needed: compile-time switch): every band
+// from KMAX before the tile's first to its last is a regular band (no image edge,
+// no forced last centre in reach), so column tau*b + j is covered by exactly
+// 1 + (2R - j) / TAU bands -- a compile-time count -- and lanes >= `own0` own
+// their columns: no shared table, no geometry loop, no CTA barrier.
+template <int TAU, int R, int C, int K, int VEC, bool INTERIOR = false>
 __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int nrw, int par0, int lane,
                                                     float* obase, long long opitch, int ncol,
-                                                    const float* inv_col) {
+                                                    const float* inv_col, int own0 = 0) {
     constexpr int M = 2 * R + 1, RW = K / M;
     constexpr int KMAX = (M - 1) / TAU;
     float acc[TAU][RW * C];
@@ -1440,12 +1455,18 @@ __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int
             for (int c = 0; c < C; ++c) acc[j][rr * C + c] += rev ? ys[rr * M + (M - 1 - j)][c] : ys[rr * M + j][c];
         }
     }
+    if (INTERIOR && lane < own0) return;  // halo bands: their columns belong to the previous tile
 #pragma unroll
     for (int j = 0; j < TAU; ++j) {
         const int xl = TAU * lane + j;
-        if (xl >= ncol) continue;
-        const float sc = inv_col[xl];
-        if (!(sc > 0.f)) continue;  // not owned by this tile
+        float sc;
+        if constexpr (INTERIOR) {
+            sc = 1.0f / (float)(1 + (2 * R - j) / TAU);  // compile-time, correctly rounded like kInvCount
+        } else {
+            if (xl >= ncol) continue;
+            sc = inv_col[xl];
+            if (!(sc > 0.f)) continue;  // not owned by this tile
+        }
         float* op = obase + (long long)xl * opitch;
         if (nrw == RW) {
 #pragma unroll
@@ -1693,9 +1714,17 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int Y0 = J * NW * RW;
     const int TR = min(NW * RW, g.Hl - Y0);  // tile rows
 
-    float* tl = sm;  // output tile [x][y*C + c] or [y][x*C + c]
+    using RL = Rec<R, C>;
+    // shared memory: [separator-map staging: warp x slot x lane x MAPP][output tile][1/count per column]
+    float* mapsm = sm + (wid * 2 * 32 + lane) * RL::MAPP;
+    float* tl = sm + NW * 2 * 32 * RL::MAPP;  // output tile [x][y*C + c] or [y][x*C + c]
     const int bl = min(B0 + 32, g.nb) - 1;
-    const int xa = band_lo(g, B0), xb = band_lo(g, bl) + M - 1;
+    // interior tile: bands B0 - KMAX .. B0 + 31 are all regular (centres r + tau*b), neither
+    // image edge nor the forced last centre reaches its columns
+    const bool interior = bxi > 0 && B0 + 32 < g.nb && B0 + 32 <= g.nreg &&
+                          (B0 + 32) * g.tau <= g.Wl - 1 - 2 * g.r;
+    const int xa = interior ? g.tau * B0 : band_lo(g, B0);
+    const int xb = (interior ? g.tau * bl : band_lo(g, bl)) + M - 1;
     const int ncol = xb - xa + 1;
     // Output tile layout.  Column-major [x][y*C + c] (pitch TP, 16-byte rows)
     // when every owned column leaves as one bulk copy; otherwise row-major
@@ -1720,7 +1749,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     std::conditional_t<(R >= SGWLS_LAZY_MIN_R), ChunkInL<R, C, CG, RW>, ChunkIn<R, C, CG, RW>> in;
     const int y0 = j * RW;
     const int nrows = active ? min(RW, g.Hl - y0) : 0;
-    const int lo = active ? band_lo(g, b) : 0;
+    const int lo = active ? (interior ? g.tau * b : band_lo(g, b)) : 0;
     const bool multi = g.P > 1 || g.has_prev || g.has_next;  // separators exist
     // ---- 0. tile geometry (column ownership, 1/count, zeroing): independent of the
     //         predecessor, so it runs before the dependent-launch wait
@@ -1729,10 +1758,24 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const bool last_cta = B0 + 32 >= g.nb;
     const bool shfl_avg = to.nph > 1 && g.tau <= 3 && bl < g.nreg &&
                           (!last_cta || (bl - B0) + div_tau(g, M - 1) <= 31);
+    // direct stores to the transposed output (no tile round trip) when the
+    // vector width divides the output rows
+    constexpr int DVEC = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
+#ifndef SGWLS_NO_DIRECT
+    // measured on B200: c1 +8.5 %, c3 +1.8 %, c5 +0.6 %; c4 (2 channels, float2 runs) -4.7 %, so
+    // only for one channel or full float4 runs
+    const bool direct = shfl_avg && !to.ratio && to.transpose_out && (C == 1 || DVEC == 4) &&
+                        ((long long)g.Hl * C) % DVEC == 0 &&
+                        (reinterpret_cast<uintptr_t>(oi) & (DVEC * 4 - 1)) == 0;
+#else
+    const bool direct = false;
+#endif
+    // interior tiles that store directly need no column table (compile-time counts, lane ownership)
+    const bool lean = direct && interior;
     // per-column averaging scale 1/count, positive if this CTA owns the column
     // (writes it out), negative otherwise
     float* inv_col = tl + ((tsize + 3) & ~3);
-    for (int xl = tid; xl < ncol; xl += NT) {
+    for (int xl = tid; xl < (lean ? 0 : ncol); xl += NT) {
         int bmin, bmax;
         covering(g, xa + xl, bmin, bmax);
         // owner CTA = ceil((bmax - 31) / step) (0 if bmax <= 31), tested without a division
@@ -1760,10 +1803,8 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         for (int i = tid; i < (tsize + 3) / 4; i += NT) reinterpret_cast<float4*>(tl)[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     // this chunk's separator maps -> shared memory (per warp: slot 0 = sigma_{j-1},
-    // slot 1 = sigma_j), asynchronously; before the wait when KA is not the predecessor
-    using RL = Rec<R, C>;
-    // per warp: [slot][lane][MAPP], 16-byte aligned
-    float* mapsm = inv_col + ((ncol + 3) & ~3) + (wid * 2 * 32 + lane) * RL::MAPP;
+    // slot 1 = sigma_j; [slot][lane][MAPP], 16-byte aligned), asynchronously; before
+    // the wait when KA is not the predecessor
     const int JA = to.nwa_shift >= 0 ? j >> to.nwa_shift : j / to.nwa, sj = j - JA * to.nwa;
     const bool lastc = (j == g.P - 1) && !g.has_next;
     const bool has_left = j > 0 || g.has_prev;
@@ -1898,24 +1939,26 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             chunk_interior_solve<R, C, CG, RW, false>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
         }
     }
+    const int par0 = y0 & 1;
+    if (lean) {  // no shared table, no barrier: counts are compile-time, lanes >= 32 - step own their columns
+        const int nrw = wid < nw ? min(RW, g.Hl - y0) : 0;
+        float* obase = oi + ((long long)xa * g.Hl + y0) * C;
+        const long long opitch = (long long)g.Hl * C;
+        const int own0 = 32 - to.step;
+        if (nrw > 0) {
+            switch (g.tau) {
+                case 1: average_shfl_direct<1, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
+                case 2: average_shfl_direct<2, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
+                default: average_shfl_direct<3, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
+            }
+        }
+        return;
+    }
     __syncthreads();
     // ---- 4. averaging into the shared output tile, fixed phase order
     //         (nph == 1: no two bands overlap, every tile cell has one writer)
     //         Values enter the tile already divided by their column's count.
-    const int par0 = y0 & 1;
     float* tbase = tl + (lo - xa) * sx + (y0 - Y0) * sy;
-    // direct stores to the transposed output (no tile round trip) when the
-    // vector width divides the output rows
-    constexpr int DVEC = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
-#ifndef SGWLS_NO_DIRECT
-    // measured on B200: c1 +8.5 %, c3 +1.8 %, c5 +0.6 %; c4 (2 channels, float2 runs) -4.7 %, so
-    // only for one channel or full float4 runs
-    const bool direct = shfl_avg && !to.ratio && to.transpose_out && (C == 1 || DVEC == 4) &&
-                        ((long long)g.Hl * C) % DVEC == 0 &&
-                        (reinterpret_cast<uintptr_t>(oi) & (DVEC * 4 - 1)) == 0;
-#else
-    const bool direct = false;
-#endif
     if (direct) {
         const int nrw = wid < nw ? min(RW, g.Hl - y0) : 0;
         float* obase = oi + ((long long)xa * g.Hl + y0) * C;
