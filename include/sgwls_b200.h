@@ -39,7 +39,7 @@ extern "C" {
 #define SGWLS_B200_OK 0
 #define SGWLS_B200_EINVAL 1       /* sgwls::Error equivalent; reference text in err */
 #define SGWLS_B200_ECUDA 2        /* CUDA runtime failure or no device */
-#define SGWLS_B200_EUNSUPPORTED 3 /* valid for the reference, outside this build's limits (r > 8, C > 4) */
+#define SGWLS_B200_EUNSUPPORTED 3 /* valid for the reference, outside this build's limits (more than 4 channels) */
 
 /* device-call flags */
 #define SGWLS_B200_SYNC 1     /* synchronize the stream and report pivot failures */

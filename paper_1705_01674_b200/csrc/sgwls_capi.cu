@@ -101,10 +101,6 @@ int validate_cfg(const sgwls_b200_config* c, std::string& msg) {
         msg = "sgwls_b200: unknown axis";
         return SGWLS_B200_EINVAL;
     }
-    if (c->r > kMaxR) {
-        msg = "sgwls_b200: r > " + std::to_string(kMaxR) + " is not supported by this build";
-        return SGWLS_B200_EUNSUPPORTED;
-    }
     return SGWLS_B200_OK;
 }
 
@@ -155,6 +151,8 @@ struct AxisPlan {
     int bx;
     int fast, step, ncta, nw, nph, nwa = 8;
     size_t rec_n, rs_n, z_n, u_n, map_n = 0;
+    int anyr = 0;      // r > kMaxR: the any-radius path (sgwls_anyr.cu)
+    size_t anyr_n = 0; // its workspace
 };
 
 
@@ -253,6 +251,15 @@ AxisPlan plan_axis(int Hl, int Wl, int C, int Cg, int r, int tau, int batch) {
         ap.u_n = 0;
         return ap;
     }
+    if (r > kMaxR) {  // beyond the templated kernels: one thread per band, whole band, runtime r
+        ap.anyr = 1;
+        g.P = 1;
+        ap.kmax = 0;
+        ap.rec_n = ap.rs_n = ap.z_n = 0;
+        ap.u_n = (size_t)batch * Hl * g.nb * g.m * C;
+        ap.anyr_n = anyr_ws_floats(g);
+        return ap;
+    }
     static const int target_pos = [] {
         const char* v = std::getenv("SGWLS_CHUNK_POS");  // tuning knob (positions per chunk)
         return v ? std::atoi(v) : kTargetChunkPositions;
@@ -280,6 +287,7 @@ int kernels_per_pass(const AxisPlan& ap) {
         // ka_tile [+ k2_tree] when the lines have several chunks; kb_tile
         return (ap.g.P > 1 ? (1 + (PS > 1 ? 1 : 0)) : 0) + 1;
     }
+    if (ap.anyr) return 2;  // k_band_anyr + k4_average
     return (ap.g.P > 1 ? 2 : 0) + 2;
 }
 
@@ -361,7 +369,15 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         u_n = mx(u_n, ap1.u_n);
     }
     const size_t img_n = (size_t)batch * W * H * C;
-    DevBuf rec, rs, z, U, bufA, bufB, gt, maps;
+    DevBuf rec, rs, z, U, bufA, bufB, gt, maps, anyws, anylut;
+    if (ap0.anyr || ap1.anyr) {
+        // any-radius path: workspace of the larger axis, lambda * spatial factor by squared distance
+        anyws.alloc(mx(need0 ? ap0.anyr_n : 0, need1 ? ap1.anyr_n : 0), st);
+        // (filled on the device: stream-ordered and safe inside a graph capture)
+        anylut.alloc(anyr_lut_floats(cfg->r), st);
+        CK(launch_anyr_lut(anylut.p, anyr_lut_floats(cfg->r), cfg->lambda, cfg->weight_kind == SGWLS_B200_WEIGHT_EXP,
+                           cfg->sigma_s, cfg->alpha_s, cfg->epsilon, st));
+    }
     maps.alloc(map_n, st);
     rec.alloc(rec_n, st);
     rs.alloc(rs_n, st);
@@ -414,6 +430,9 @@ void run_smooth(const float* d_t, const float* d_g, int batch, int W, int H, int
         pl.U = U.p;
         pl.err = (p == 0) ? d_err : nullptr;
         pl.w = &wd;
+        pl.anyr = ap.anyr;
+        pl.anyr_ws = anyws.p;
+        pl.anyr_lspat = anylut.p;
         if (sh && p == 0 && sh->d_mask) pl.geom.msk = sh->d_mask;
         if (sh && lastp && sh->ratio) {
             pl.ratio = 1;
@@ -931,7 +950,7 @@ int sgwls_b200_kernel_launches(int width, int height, int channels, int gch, int
 }
 
 int sgwls_b200_describe_pass(int extent, int sweep, int r, int tau, int* info, int* centers, int cap) {
-    if (extent < 1 || sweep < 1 || r < 1 || r > kMaxR || tau < 1) return -1;
+    if (extent < 1 || sweep < 1 || r < 1 || tau < 1) return -1;
     const AxisPlan ap = plan_axis(sweep, extent, 1, 1, r, tau, 1);
     if (info) {
         info[0] = ap.g.nb;

@@ -156,6 +156,11 @@ __device__ __forceinline__ float guidance_weight_k(const WeightDev& W, float ran
 // MUFU per edge instead of FMUL, MUFU and two more FMULs.
 template <int WK>
 __device__ __forceinline__ float guidance_lweight_k(const WeightDev& W, float range2, int d2) {
+#ifdef SGWLS_EXPERIMENT_FREE_WEIGHTS
+    // timing experiment only (factor reuse): every edge weight costs nothing,
+    // the upper bound of what re-reading stored weights in passes 3/4 could save
+    return W.lam;
+#endif
     if constexpr (WK == 1) {
         return fast_ex2(fmaf(range2, W.exp_k, W.lg2ls[d2]));
     } else {

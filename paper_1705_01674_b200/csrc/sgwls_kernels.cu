@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(256) k_validate_sparse(const float* __restrict
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st) {
     ProfScope ps("pass", st);
+    if (pl.anyr) return launch_pass_anyr(pl, st);
     if (pl.fast) {
         switch (pl.geom.r) {
             case 1: return tile::launch_tile_r<1>(pl, st);

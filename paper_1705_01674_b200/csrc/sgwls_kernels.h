@@ -44,9 +44,20 @@ struct PassLaunch {
     float* zg = nullptr;   // nslab-1 slab separators
     float* bsg = nullptr;  // their back-substitution rows
     float* grec = nullptr; // group records of the slab (phase A -> B), kSlabWarps x REC per band
+    // any-radius path (r > kMaxR, sgwls_anyr.cu): line-interleaved workspace and the
+    // lambda * spatial-factor table by squared distance (device)
+    int anyr = 0;
+    float* anyr_ws = nullptr;
+    const float* anyr_lspat = nullptr;
 };
 
 cudaError_t launch_pass(const PassLaunch& pl, cudaStream_t st);
+cudaError_t launch_pass_anyr(const PassLaunch& pl, cudaStream_t st);
+size_t anyr_ws_floats(const PassGeom& g);
+size_t anyr_lut_floats(int r);
+// lut[d2] = lambda * spatial factor of squared distance d2 (proj/src/weights.cpp:55-71), in double then rounded
+cudaError_t launch_anyr_lut(float* lut, size_t n, double lambda, bool exp_kind, double sigma_s, double alpha_s,
+                            double eps, cudaStream_t st);
 size_t rec_floats(int r, int C);
 size_t rs_floats(int r, int C);
 size_t map_floats(int r, int C);

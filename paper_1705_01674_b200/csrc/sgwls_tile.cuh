@@ -65,6 +65,41 @@ __device__ __forceinline__ void bulk_commit_and_wait_read() {
 // order this thread's generic-proxy shared-memory writes before async-proxy reads
 __device__ __forceinline__ void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+// Bulk (TMA) global -> shared copy completing on an mbarrier; 16-byte aligned
+// addresses, size % 16 == 0.  One instruction moves a whole row segment: no
+// per-lane loads, no L1 wavefronts.
+__device__ __forceinline__ void bulk_g2s(float* sdst, const float* gsrc, unsigned bytes, unsigned long long* mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            (unsigned)__cvta_generic_to_shared(sdst)),
+        "l"(gsrc), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(mbar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* mbar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(mbar)), "r"(count)
+                 : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* mbar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(mbar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "MBAR_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@p bra MBAR_DONE;\n"
+        "bra MBAR_WAIT;\n"
+        "MBAR_DONE:\n"
+        "}" ::"r"((unsigned)__cvta_generic_to_shared(mbar)),
+        "r"(parity)
+        : "memory");
+}
+
 // 16-byte asynchronous global -> shared copy (LDGSTS: no registers held while in flight)
 __device__ __forceinline__ void cp_async16(float* sdst, const float* gsrc) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"((unsigned)__cvta_generic_to_shared(sdst)),
@@ -332,6 +367,50 @@ __device__ __forceinline__ void load_chunk_lazy(ChunkInL<R, C, CG, RW>& in, cons
         rowF += stF;
         rowG += stG;
         if (split) rowM += g.Wl;
+    }
+}
+
+// Same, from the CTA's staged rows in shared memory (kb_tile, bulk-copied row
+// segments): sFr / sGr point at this lane's first sample of the chunk's first
+// row (sGr: one row above it is the previous row), pf / pg are the row pitches.
+template <int R, int C, int CG, int RW, bool FULLC>
+__device__ __forceinline__ void load_chunk_lazy_staged(ChunkInL<R, C, CG, RW>& in, const float* sFr, int pf,
+                                                       const float* sGr, int pg, const PassGeom& g, int y0,
+                                                       int nrows) {
+    constexpr int M = 2 * R + 1;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+        const int jj = M - R + i;
+        const int y = y0 - 1;
+        if (y >= 0) {
+            const int co = (y & 1) ? (M - 1 - jj) : jj;
+#pragma unroll
+            for (int c = 0; c < CG; ++c) in.gprev[i][c] = sGr[-pg + co * CG + c];
+        } else {
+#pragma unroll
+            for (int c = 0; c < CG; ++c) in.gprev[i][c] = 0.f;
+        }
+    }
+#pragma unroll
+    for (int rr = 0; rr < RW; ++rr) {
+        const bool valid = FULLC || rr < nrows;
+        const bool odd = (RW % 2 == 0) ? ((rr & 1) != 0) : (((y0 + rr) & 1) != 0);
+        float vf[M][C], vg[M][CG];
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+#pragma unroll
+            for (int c = 0; c < C; ++c) vf[jj][c] = valid ? sFr[rr * pf + jj * C + c] : 0.f;
+#pragma unroll
+            for (int c = 0; c < CG; ++c) vg[jj][c] = valid ? sGr[rr * pg + jj * CG + c] : 0.f;
+        }
+#pragma unroll
+        for (int jj = 0; jj < M; ++jj) {
+            const int k = rr * M + jj;
+#pragma unroll
+            for (int c = 0; c < C; ++c) in.f[k][c] = odd ? vf[M - 1 - jj][c] : vf[jj][c];
+#pragma unroll
+            for (int c = 0; c < CG; ++c) in.gp[k][c] = odd ? vg[M - 1 - jj][c] : vg[jj][c];
+        }
     }
 }
 
@@ -1487,6 +1566,10 @@ __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int
     }
 }
 
+// row pitch (floats) of kb_tile's staged rows: up to 3 floats of alignment slack in
+// front of the tile's 31*tau + M columns, rounded to whole 16-byte vectors
+__host__ __device__ constexpr int kb_stage_pitch(int tau, int M, int ch) { return (3 + (31 * tau + M) * ch + 3) & ~3; }
+
 struct TileOut {
     float* out;
     int transpose_out;
@@ -1502,6 +1585,10 @@ struct TileOut {
     int ratio;
     float floor_;
     float* und;
+    // the CTA stages its input rows (image + guidance) in shared memory with one bulk
+    // (TMA) copy per row segment instead of per-lane loads (r >= 2, packed input,
+    // no row-slab neighbours, 16-byte aligned rows; decided on the host)
+    int stage;
 };
 
 // 1/n correctly rounded (what 1.0f / n gives) for the band count of a column, n <= 2r + 2 <= 10
@@ -1717,7 +1804,13 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     using RL = Rec<R, C>;
     // shared memory: [separator-map staging: warp x slot x lane x MAPP][output tile][1/count per column]
     float* mapsm = sm + (wid * 2 * 32 + lane) * RL::MAPP;
-    float* tl = sm + NW * 2 * 32 * RL::MAPP;  // output tile [x][y*C + c] or [y][x*C + c]
+    // staged input rows: [mbarrier, 16 B][image rows NW*RW x PF][guidance rows (1 + NW*RW) x PG]
+    const bool stage = (R >= SGWLS_LAZY_MIN_R) && to.stage != 0;
+    const int PF = stage ? kb_stage_pitch(g.tau, M, C) : 0, PG = stage ? kb_stage_pitch(g.tau, M, CG) : 0;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + NW * 2 * 32 * RL::MAPP);
+    float* sF = sm + NW * 2 * 32 * RL::MAPP + 4;
+    float* sG = sF + NW * RW * PF;
+    float* tl = stage ? sG + (NW * RW + 1) * PG : sm + NW * 2 * 32 * RL::MAPP;  // output tile [x][y*C + c] or [y][x*C + c]
     const int bl = min(B0 + 32, g.nb) - 1;
     // interior tile: bands B0 - KMAX .. B0 + 31 are all regular (centres r + tau*b), neither
     // image edge nor the forced last centre reaches its columns
@@ -1744,6 +1837,61 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int sx = colmaj ? TP : C, sy = colmaj ? C : XP;  // tile strides of x and y
     const int tsize = colmaj ? ncol * TP : TR * XP;
 
+    // ---- 0b. staged input: warp 0 issues one bulk copy per image / guidance row of the
+    //          tile (segment [xa, xb] widened to 16-byte bounds; the rows of the pass
+    //          input are complete before KA began, so this precedes the dependent-launch wait)
+    int xoF = 0, xoG = 0;
+    if (stage) {
+        const long long eF = ((long long)img * g.Hl * g.Wl + xa) * C, eG = ((long long)img * g.Hl * g.Wl + xa) * CG;
+        // element offset of column xa in a row is the same modulo 4 for every row ((Wl*C) % 4 == 0)
+        xoF = (int)(eF & 3);
+        xoG = (int)(eG & 3);
+        if (tid == 0) mbar_init(mbar, 1);
+        __syncthreads();
+        if (wid == 0) {
+            const int nrF = TR, nrG = TR + (Y0 > 0 ? 1 : 0);
+            const long long endF = (long long)g.batch * g.img_stride, endG = (long long)g.batch * g.gimg_stride;
+            auto seg = [&](long long e0, int xo, int cnt, long long end, long long& a) {
+                a = e0 - xo;
+                long long len = (xo + cnt + 3) & ~3;
+                if (a + len > end) len = end - a;
+                return (unsigned)(len * 4);
+            };
+            long long aF0, aG0;
+            const unsigned bF = seg(eF + (long long)Y0 * g.Wl * C, xoF, ncol * C, endF, aF0);
+            const unsigned bG = seg(eG + (long long)Y0 * g.Wl * CG, xoG, ncol * CG, endG, aG0);
+            // the clamp can only bite in the image's very last row: count it exactly
+            unsigned total = 0;
+            for (int i = lane; i < nrF + nrG; i += 32) {
+                const bool isF = i < nrF;
+                const int rrow = isF ? i : i - nrF - (Y0 > 0 ? 1 : 0);  // row relative to Y0 (guidance: from -1)
+                long long a;
+                const unsigned by = isF ? seg(eF + (long long)(Y0 + rrow) * g.Wl * C, xoF, ncol * C, endF, a)
+                                        : seg(eG + (long long)(Y0 + rrow) * g.Wl * CG, xoG, ncol * CG, endG, a);
+                total += by;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+            if (lane == 0) mbar_arrive_expect_tx(mbar, total);
+            __syncwarp();
+            for (int i = lane; i < nrF + nrG; i += 32) {
+                const bool isF = i < nrF;
+                const int rrow = isF ? i : i - nrF - (Y0 > 0 ? 1 : 0);
+                long long a;
+                if (isF) {
+                    const unsigned by = seg(eF + (long long)(Y0 + rrow) * g.Wl * C, xoF, ncol * C, endF, a);
+                    bulk_g2s(sF + rrow * PF, src + a, by, mbar);
+                } else {
+                    const unsigned by = seg(eG + (long long)(Y0 + rrow) * g.Wl * CG, xoG, ncol * CG, endG, a);
+                    bulk_g2s(sG + (rrow + 1) * PG, guid + a, by, mbar);
+                }
+            }
+            (void)bF;
+            (void)bG;
+            (void)aF0;
+            (void)aG0;
+        }
+    }
     // ---- 1. chunk inputs and edge weights before the dependent-launch wait:
     //         the pass input was complete before KA began
     std::conditional_t<(R >= SGWLS_LAZY_MIN_R), ChunkInL<R, C, CG, RW>, ChunkIn<R, C, CG, RW>> in;
@@ -1826,7 +1974,16 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     };
     if (to.early) fetch_maps();
     if constexpr (R >= SGWLS_LAZY_MIN_R) {
+    if (stage) mbar_wait(mbar, 0);  // every thread: the staged rows have landed
     if (active) {
+        if (stage) {
+            const float* sFr = sF + (y0 - Y0) * PF + xoF + (lo - xa) * C;
+            const float* sGr = sG + (y0 - Y0 + 1) * PG + xoG + (lo - xa) * CG;
+            if (nrows == RW)
+                load_chunk_lazy_staged<R, C, CG, RW, true>(in, sFr, PF, sGr, PG, g, y0, nrows);
+            else
+                load_chunk_lazy_staged<R, C, CG, RW, false>(in, sFr, PF, sGr, PG, g, y0, nrows);
+        } else {
         const long long npx = (long long)g.Hl * g.Wl;
         const float* Msk = (C > 1 && g.msk != nullptr) ? g.msk + img * npx : nullptr;
         const float* F = src + img * (Msk ? npx * (C > 1 ? C - 1 : 1) : g.img_stride);
@@ -1834,6 +1991,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
             load_chunk_lazy<R, C, CG, RW, true>(in, F, Msk, guid + img * g.gimg_stride, g, lo, y0, nrows);
         else
             load_chunk_lazy<R, C, CG, RW, false>(in, F, Msk, guid + img * g.gimg_stride, g, lo, y0, nrows);
+        }
         if (err != nullptr) {  // NaN guidance: the reference's pivot failure (rare path locates it)
             float acc = 0.f;
 #pragma unroll
@@ -2102,10 +2260,11 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
 // =========================================================== host helpers
 
 template <int R, int C>
-__host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol) {
+__host__ inline size_t kb_smem_bytes(int NW, int TR, int ncol, int stage_floats = 0) {
     const int n4 = (TR * C + 3) & ~3;
     const size_t tile = (size_t)ncol * (n4 + (n4 % 8 == 0 ? 4 : 8));
-    return (((tile + 3) & ~(size_t)3) + ((ncol + 3) & ~3) + (size_t)NW * 2 * Rec<R, C>::MAPP * 32) * sizeof(float);
+    return (((tile + 3) & ~(size_t)3) + ((ncol + 3) & ~3) + (size_t)NW * 2 * Rec<R, C>::MAPP * 32 + stage_floats) *
+           sizeof(float);
 }
 
 
@@ -2205,13 +2364,29 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         ProfScope ps("kb_tile", st);
         constexpr int RW = rows_per_chunk(R, C);
         const int ncol = 31 * g.tau + 2 * g.r + 1;
-        const size_t smem = kb_smem_bytes<R, C>(NW, NW * RW, ncol);
+        // staged input rows (bulk copies): lazy-weight radii, packed input, no slab neighbours,
+        // rows and bases on 16-byte bounds
+        static const int stage_env = [] {
+            // schedule knob: 1 = stage the tile's rows with bulk copies.  Measured on B200 with one
+            // bulk copy per row segment (33 per CTA): c5 KB +15 %, c4 +3 %, c3 +9 % SLOWER than
+            // per-lane loads, so off by default
+            const char* v = std::getenv("SGWLS_KB_STAGE");
+            return v ? std::atoi(v) : 0;
+        }();
+        const bool stage = stage_env && R >= SGWLS_LAZY_MIN_R && !slab && g.msk == nullptr &&
+                           ((long long)g.Wl * C) % 4 == 0 && ((long long)g.Wl * CG) % 4 == 0 &&
+                           (reinterpret_cast<uintptr_t>(pl.src) & 15) == 0 &&
+                           (reinterpret_cast<uintptr_t>(pl.guid) & 15) == 0;
+        const int M = 2 * R + 1;
+        const int stage_floats =
+            stage ? 4 + NW * RW * kb_stage_pitch(g.tau, M, C) + (NW * RW + 1) * kb_stage_pitch(g.tau, M, CG) : 0;
+        const size_t smem = kb_smem_bytes<R, C>(NW, NW * RW, ncol, stage_floats);
         // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
         // triggering) or, with a single KA tile per band, KA itself
         const bool early = slab || PSA > 1;
         const int nwa_shift = (NWA & (NWA - 1)) == 0 ? __builtin_ctz((unsigned)NWA) : -1;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, nwa_shift, pl.ratio,
-                   pl.ratio_floor, pl.und};
+                   pl.ratio_floor, pl.und, stage ? 1 : 0};
         const dim3 kgrid(pl.ncta, PB, g.batch);
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

@@ -84,9 +84,12 @@ def test_shape_errors():
         S.smooth(np.zeros((0, 4), np.float32), np.zeros((0, 4), np.float32))
 
 
-def test_unsupported_radius_is_reported():
-    with pytest.raises(S.Error, match="r > 8"):
-        S.validate(S.SmoothConfig(r=9, tau=1))
+def test_any_radius_validates_like_the_reference():
+    """proj/src/smoother.cpp:105-107: every r >= 1 is valid (r > 8 runs the any-radius path)"""
+    S.validate(S.SmoothConfig(r=9, tau=1))
+    S.validate(S.SmoothConfig(r=40, tau=81))
+    with pytest.raises(S.Error, match=r"smooth: tau must be in \[1, 2r\+1\], got 82"):
+        S.validate(S.SmoothConfig(r=40, tau=82))
 
 
 @pytest.mark.skipif(__import__("conftest").HAS_CUDA, reason="CPU-only check")

@@ -57,6 +57,12 @@ CASES = [
     (80, 50, 1, 1, 400.0, 8, 8, 2, 1, 0),
     (300, 257, 1, 1, 900.0, 1, 1, 4, 1, 0),
     (257, 300, 3, 1, 400.0, 2, 5, 4, 1, 1),
+    # r > 8: the any-radius path (sgwls_anyr.cu); the reference takes every r >= 1
+    (60, 70, 1, 1, 400.0, 9, 5, 2, 1, 0),
+    (50, 90, 3, 3, 900.0, 12, 25, 3, 0, 1),
+    (40, 45, 2, 1, 200.0, 20, 7, 2, 1, 0),   # one axis clipped (45 < 2r+1 on neither, 40 < 41 on the row pass)
+    (9, 30, 1, 1, 300.0, 16, 33, 4, 1, 0),   # both extents below 2r+1: single clipped bands
+    (64, 100, 1, 2, 100.0, 10, 1, 1, 0, 1),
 ]
 
 
@@ -291,3 +297,22 @@ def test_c4_batch_parity_16_pairs(port):
         assert (und[k] == wund).all(), ids[k]
     print(f"c4 pairs {ids}: max|d| = {worst:.3g}")
     assert worst <= TOL
+
+
+def test_any_radius_sparse_and_pivot_error(port):
+    """r > 8 through interpolate_sparse (pack / ratio kernels around the any-radius passes)
+    and the reference's pivot failure on NaN guidance"""
+    rng = np.random.default_rng(99)
+    h, w = 48, 56
+    g = _piecewise(rng, h, w, 1)[:, :, 0]
+    mask = (rng.uniform(size=(h, w)) < 0.1).astype(np.float32)
+    vals = (_piecewise(rng, h, w, 1)[:, :, 0] * mask).astype(np.float32)
+    cfg = _cfg(300.0, 10, 6, 2, 1, 0)
+    want, und_w = port.interpolate_sparse(vals, mask, g, cfg)
+    got, und = S.interpolate_sparse(S.SparseField(vals, mask), g, cfg, return_undefined=True)
+    assert np.abs(got.astype(np.float64) - want.reshape(got.shape)).max() <= TOL
+    assert np.array_equal(und.reshape(und_w.shape) != 0, und_w != 0)
+    gbad = g.copy()
+    gbad[20, 30] = np.nan
+    with pytest.raises(S.Error, match="non-positive pivot"):
+        S.smooth(vals, gbad, cfg)
