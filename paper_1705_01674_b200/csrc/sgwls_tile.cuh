@@ -30,9 +30,11 @@
 // All eliminations: magnitudes + row-sum pivots (sgwls_device.cuh).
 #pragma once
 
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched through the runtime)
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <type_traits>
 #include <utility>
 
@@ -75,6 +77,45 @@ __device__ __forceinline__ void bulk_g2s(float* sdst, const float* gsrc, unsigne
         "l"(gsrc), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(mbar))
         : "memory");
 }
+// Tiled (tensor-map) TMA load of a 2-D box: element coordinates (x, y) of the box's
+// first element, out-of-bounds elements arrive as zeros; 128-byte aligned destination.
+__device__ __forceinline__ void tma_load_2d(float* sdst, const CUtensorMap* tm, int x, int y,
+                                            unsigned long long* mbar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+            "r"((unsigned)__cvta_generic_to_shared(sdst)),
+        "l"(tm), "r"(x), "r"(y), "r"((unsigned)__cvta_generic_to_shared(mbar))
+        : "memory");
+}
+
+// Tensor map over `rows` rows of `row_elems` fp32 each (row pitch = row_elems), box
+// box_w x box_h, no swizzle, zero fill.  False when the driver entry point is missing
+// or the layout is outside TMA's rules (16-byte base and pitch, box sides <= 256).
+inline bool encode_rows_map(CUtensorMap* tm, const float* base, long long row_elems, long long rows, int box_w,
+                            int box_h) {
+    typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static EncodeFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return (EncodeFn)p;
+    }();
+    if (!fn || box_w > 256 || box_h > 256 || (box_w % 4) != 0 || (row_elems % 4) != 0 ||
+        (reinterpret_cast<uintptr_t>(base) & 15) != 0)
+        return false;
+    const cuuint64_t gdim[2] = {(cuuint64_t)row_elems, (cuuint64_t)rows};
+    const cuuint64_t gstr[1] = {(cuuint64_t)row_elems * sizeof(float)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)box_h};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), gdim, gstr, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 __device__ __forceinline__ void mbar_init(unsigned long long* mbar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(mbar)), "r"(count)
                  : "memory");
@@ -1203,7 +1244,7 @@ __device__ __forceinline__ void k2_tree_body(const PassGeom& g, const float* rec
 template <int R, int C, int MAXT>
 __global__ void __launch_bounds__(MAXT) k2_tree(const PassGeom g, const float* __restrict__ rec,
                                                float* __restrict__ rsc, float* __restrict__ z, int staged) {
-    extern __shared__ float sm[];
+    extern __shared__ __align__(128) float sm[];
     pdl_wait();     // KA's records
     pdl_trigger();  // KB may launch now: everything it reads before its own wait (KA's output) is complete
     k2_tree_body<R, C>(g, rec, rsc, z, sm, threadIdx.x, threadIdx.y, blockDim.y, blockIdx.x, staged != 0);
@@ -1294,7 +1335,7 @@ __global__ void SGWLS_KA_BOUNDS ka_tile(const PassGeom g, const float* __restric
                                                const float* __restrict__ guid, float* __restrict__ srec,
                                                float* __restrict__ maps, const __grid_constant__ WeightDev W, int NW) {
     using RL = Rec<R, C>;
-    extern __shared__ float sm[];
+    extern __shared__ __align__(128) float sm[];
     // NW chunks per tile, NWK (= blockDim.y <= NW) warps: each warp runs
     // chunks wid, wid + NWK, ...  Fewer warps than chunks shrink the share of
     // warps idling while warp 0 reduces the tile (with one warp per chunk, ncu
@@ -1634,7 +1675,7 @@ template <int R, int C>
 __global__ void __launch_bounds__(512) k2_slab_reduce(const PassGeom g, int PS, const float* __restrict__ srec,
                                                       float* __restrict__ grec, float* __restrict__ slabrec) {
     using RL = Rec<R, C>;
-    extern __shared__ float sm[];
+    extern __shared__ __align__(128) float sm[];
     const int lane = threadIdx.x, w = threadIdx.y, NG = blockDim.y;
     const int NL = g.nb * g.batch;
     const long long NLl = NL;
@@ -1669,7 +1710,7 @@ __global__ void __launch_bounds__(512) k2_slab_solve(const PassGeom g, int PS, i
                                                      float* __restrict__ bsg, float* __restrict__ rsc,
                                                      float* __restrict__ z) {
     using RL = Rec<R, C>;
-    extern __shared__ float sm[];
+    extern __shared__ __align__(128) float sm[];
     const int lane = threadIdx.x, w = threadIdx.y, NG = blockDim.y;
     const int NL = g.nb * g.batch;
     const long long NLl = NL;
@@ -1780,10 +1821,12 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                                                const float* __restrict__ guid, const float* __restrict__ zsep,
                                                const float* __restrict__ maps, const TileOut to,
                                                unsigned long long* __restrict__ err,
-                                               const __grid_constant__ WeightDev W) {
+                                               const __grid_constant__ WeightDev W,
+                                               const __grid_constant__ CUtensorMap tmF,
+                                               const __grid_constant__ CUtensorMap tmG) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1, K = RW * M;
-    extern __shared__ float sm[];
+    extern __shared__ __align__(128) float sm[];
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
     const int tid = wid * 32 + lane, NT = NW * 32;
     // grid: (band tile, chunk tile, image)
@@ -1808,9 +1851,10 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const bool stage = (R >= SGWLS_LAZY_MIN_R) && to.stage != 0;
     const int PF = stage ? kb_stage_pitch(g.tau, M, C) : 0, PG = stage ? kb_stage_pitch(g.tau, M, CG) : 0;
     unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + NW * 2 * 32 * RL::MAPP);
-    float* sF = sm + NW * 2 * 32 * RL::MAPP + 4;
-    float* sG = sF + NW * RW * PF;
-    float* tl = stage ? sG + (NW * RW + 1) * PG : sm + NW * 2 * 32 * RL::MAPP;  // output tile [x][y*C + c] or [y][x*C + c]
+    float* sF = sm + NW * 2 * 32 * RL::MAPP + 32;
+    float* sG = sF + ((NW * RW * PF + 31) & ~31);
+    float* tl = stage ? sG + (((NW * RW + 1) * PG + 31) & ~31)
+                      : sm + NW * 2 * 32 * RL::MAPP;  // output tile [x][y*C + c] or [y][x*C + c]
     const int bl = min(B0 + 32, g.nb) - 1;
     // interior tile: bands B0 - KMAX .. B0 + 31 are all regular (centres r + tau*b), neither
     // image edge nor the forced last centre reaches its columns
@@ -1846,9 +1890,17 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         // element offset of column xa in a row is the same modulo 4 for every row ((Wl*C) % 4 == 0)
         xoF = (int)(eF & 3);
         xoG = (int)(eG & 3);
-        if (tid == 0) mbar_init(mbar, 1);
+        if (tid <= NW) mbar_init(mbar + tid, 1);  // [0]: the tile's rows; [1 + w]: warp w's separator maps
         __syncthreads();
-        if (wid == 0) {
+        if (to.stage == 2) {  // two tensor-map boxes: the tile's image rows, its guidance rows from Y0 - 1
+            // the box's first element must sit on a 16-byte boundary: start up to 3 floats early
+            // (the pitch has that slack), xoF / xoG skip them
+            if (tid == 0) {
+                mbar_arrive_expect_tx(mbar, (unsigned)((NW * RW * PF + (NW * RW + 1) * PG) * sizeof(float)));
+                tma_load_2d(sF, &tmF, xa * C - xoF, img * g.Hl + Y0, mbar);
+                tma_load_2d(sG, &tmG, xa * CG - xoG, img * g.Hl + Y0 - 1, mbar);
+            }
+        } else if (wid == 0) {
             const int nrF = TR, nrG = TR + (Y0 > 0 ? 1 : 0);
             const long long endF = (long long)g.batch * g.img_stride, endG = (long long)g.batch * g.gimg_stride;
             auto seg = [&](long long e0, int xo, int cnt, long long end, long long& a) {
@@ -1958,7 +2010,23 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const bool has_left = j > 0 || g.has_prev;
     const bool r_inner = !lastc && sj < to.nwa - 1 && j < g.P - 1;  // sigma_j inner in KA tile JA
     const bool l_inner = sj > 0;  // sigma_{j-1} inner in the same KA tile
+    // staged mode: the warp's 32 maps of a separator are one contiguous run
+    // ([chunk][line][MAPP]), moved by ONE bulk copy per slot onto the warp's own mbarrier
+    unsigned long long* mbar_w = mbar + 1 + wid;
     auto fetch_maps = [&]() {
+        if (stage) {
+            if (lane == 0 && wid < nw && multi && (l_inner || r_inner)) {
+                const long long L0 = (long long)img * g.nb + B0;
+                const int nl = (int)min((long long)32, NLl - L0);
+                const unsigned by = (unsigned)(nl * RL::MAPP * sizeof(float));
+                const float* gp0 = maps + ((long long)j * NLl + L0) * RL::MAPP;
+                float* dst = sm + wid * 2 * 32 * RL::MAPP;
+                mbar_arrive_expect_tx(mbar_w, by * ((l_inner ? 1 : 0) + (r_inner ? 1 : 0)));
+                if (l_inner) bulk_g2s(dst, gp0 - NLl * RL::MAPP, by, mbar_w);
+                if (r_inner) bulk_g2s(dst + 32 * RL::MAPP, gp0, by, mbar_w);
+            }
+            return;
+        }
         if (!(active && multi)) return;
         const float* gp = maps + ((long long)j * NLl + L) * RL::MAPP;
         if (l_inner) {
@@ -2047,7 +2115,11 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                 zA[q][c] = hA ? zb[((long long)(q - R) * C + c) * NLl] : 0.f;
                 zB[q][c] = hB ? zb[(q * C + c) * NLl] : 0.f;
             }
-        cp_async_wait_all();  // this lane's own map columns (no cross-lane reads: no warp barrier)
+        if (stage) {
+            if (l_inner || r_inner) mbar_wait(mbar_w, 0);
+        } else {
+            cp_async_wait_all();  // this lane's own map columns (no cross-lane reads: no warp barrier)
+        }
         if (r_inner) {
             apply_map<R, C>(mapsm + 32 * RL::MAPP, zA, zB, zr);
         } else if (!lastc) {
@@ -2367,31 +2439,45 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         // staged input rows (bulk copies): lazy-weight radii, packed input, no slab neighbours,
         // rows and bases on 16-byte bounds
         static const int stage_env = [] {
-            // schedule knob: 1 = stage the tile's rows with bulk copies.  Measured on B200 with one
-            // bulk copy per row segment (33 per CTA): c5 KB +15 %, c4 +3 %, c3 +9 % SLOWER than
-            // per-lane loads, so off by default
+            // schedule knob: 0 = per-lane loads; 1 = one bulk copy per row segment (33 per CTA:
+            // measured c5 KB +15 %, c4 +3 %, c3 +9 % SLOWER than per-lane loads); 2 = one tensor-map
+            // box per array
             const char* v = std::getenv("SGWLS_KB_STAGE");
-            return v ? std::atoi(v) : 0;
+            return v ? std::atoi(v) : -1;
         }();
-        const bool stage = stage_env && R >= SGWLS_LAZY_MIN_R && !slab && g.msk == nullptr &&
+        // default: tensor-map staging (mode 2) for r = 2 -- measured c5 +3.4 %, c4 +2.6 %; c3 (r = 3,
+        // 8-row tiles) -1.9 %, so r >= 3 keeps the per-lane loads
+        const int stage_sel = stage_env >= 0 ? stage_env : (R == 2 ? 2 : 0);
+        const bool stage = stage_sel && R >= SGWLS_LAZY_MIN_R && !slab && g.msk == nullptr &&
                            ((long long)g.Wl * C) % 4 == 0 && ((long long)g.Wl * CG) % 4 == 0 &&
                            (reinterpret_cast<uintptr_t>(pl.src) & 15) == 0 &&
                            (reinterpret_cast<uintptr_t>(pl.guid) & 15) == 0;
         const int M = 2 * R + 1;
-        const int stage_floats =
-            stage ? 4 + NW * RW * kb_stage_pitch(g.tau, M, C) + (NW * RW + 1) * kb_stage_pitch(g.tau, M, CG) : 0;
+        const int PFh = kb_stage_pitch(g.tau, M, C), PGh = kb_stage_pitch(g.tau, M, CG);
+        const int stage_floats = stage ? 32 + ((NW * RW * PFh + 31) & ~31) + (((NW * RW + 1) * PGh + 31) & ~31) : 0;
         const size_t smem = kb_smem_bytes<R, C>(NW, NW * RW, ncol, stage_floats);
+        // mode 2: one tensor-map box per array and CTA instead of one bulk copy per row
+        CUtensorMap tmF, tmG;
+        std::memset(&tmF, 0, sizeof tmF);
+        std::memset(&tmG, 0, sizeof tmG);
+        int stage_mode = stage ? 1 : 0;
+        if (stage && stage_sel == 2)  // no tensor map (box side > 256, no driver entry point): per-lane loads
+            stage_mode =
+                (encode_rows_map(&tmF, pl.src, (long long)g.Wl * C, (long long)g.batch * g.Hl, PFh, NW * RW) &&
+                 encode_rows_map(&tmG, pl.guid, (long long)g.Wl * CG, (long long)g.batch * g.Hl, PGh, NW * RW + 1))
+                    ? 2
+                    : 0;
         // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
         // triggering) or, with a single KA tile per band, KA itself
         const bool early = slab || PSA > 1;
         const int nwa_shift = (NWA & (NWA - 1)) == 0 ? __builtin_ctz((unsigned)NWA) : -1;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, nwa_shift, pl.ratio,
-                   pl.ratio_floor, pl.und, stage ? 1 : 0};
+                   pl.ratio_floor, pl.und, stage_mode};
         const dim3 kgrid(pl.ncta, PB, g.batch);
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         e = launch_pdl(kb_tile<R, C, CG>, kgrid, dim3(32, NW), smem, st, g, pl.src, pl.guid, (const float*)pl.z,
-                       (const float*)pl.maps, to, pl.err, *pl.w);
+                       (const float*)pl.maps, to, pl.err, *pl.w, tmF, tmG);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
