@@ -88,6 +88,14 @@ __device__ __forceinline__ void tma_load_2d(float* sdst, const CUtensorMap* tm, 
         : "memory");
 }
 
+// Tiled TMA store of a dense shared-memory box to (x, y) of the tensor; elements past the
+// tensor's bounds are dropped.  Bulk-group completion (bulk_commit_and_wait_read).
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int x, int y, const float* ssrc) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tm), "r"(x),
+                 "r"(y), "r"((unsigned)__cvta_generic_to_shared(ssrc))
+                 : "memory");
+}
+
 // Tensor map over `rows` rows of `row_elems` fp32 each (row pitch = row_elems), box
 // box_w x box_h, no swizzle, zero fill.  False when the driver entry point is missing
 // or the layout is outside TMA's rules (16-byte base and pitch, box sides <= 256).
@@ -1548,7 +1556,9 @@ __device__ __forceinline__ void average_shfl(const float (&ys)[K][C], int nrw, i
 template <int TAU, int R, int C, int K, int VEC, bool INTERIOR = false>
 __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int nrw, int par0, int lane,
                                                     float* obase, long long opitch, int ncol,
-                                                    const float* inv_col, int own0 = 0) {
+                                                    const float* inv_col, int own0 = 0, float* wtile = nullptr) {
+    // wtile (INTERIOR, full chunk, 4-float runs): the owned columns' runs go to the warp's
+    // shared tile [column][4] (conflict-free 16-byte stores) for ONE tensor-map store by the caller
     constexpr int M = 2 * R + 1, RW = K / M;
     constexpr int KMAX = (M - 1) / TAU;
     float acc[TAU][RW * C];
@@ -1582,6 +1592,13 @@ __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int
         float sc;
         if constexpr (INTERIOR) {
             sc = 1.0f / (float)(1 + (2 * R - j) / TAU);  // compile-time, correctly rounded like kInvCount
+            if constexpr (RW * C == 4) {
+                if (wtile != nullptr) {
+                    *reinterpret_cast<float4*>(wtile + (TAU * (lane - own0) + j) * 4) =
+                        make_float4(acc[j][0] * sc, acc[j][1] * sc, acc[j][2] * sc, acc[j][3] * sc);
+                    continue;
+                }
+            }
         } else {
             if (xl >= ncol) continue;
             sc = inv_col[xl];
@@ -1630,6 +1647,8 @@ struct TileOut {
     // (TMA) copy per row segment instead of per-lane loads (r >= 2, packed input,
     // no row-slab neighbours, 16-byte aligned rows; decided on the host)
     int stage;
+    // interior tiles send each warp's owned 4-float column runs with one tensor-map store
+    int tstore;
 };
 
 // 1/n correctly rounded (what 1.0f / n gives) for the band count of a column, n <= 2r + 2 <= 10
@@ -1823,7 +1842,8 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                                                unsigned long long* __restrict__ err,
                                                const __grid_constant__ WeightDev W,
                                                const __grid_constant__ CUtensorMap tmF,
-                                               const __grid_constant__ CUtensorMap tmG) {
+                                               const __grid_constant__ CUtensorMap tmG,
+                                               const __grid_constant__ CUtensorMap tmO) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1, K = RW * M;
     extern __shared__ __align__(128) float sm[];
@@ -2175,11 +2195,23 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         float* obase = oi + ((long long)xa * g.Hl + y0) * C;
         const long long opitch = (long long)g.Hl * C;
         const int own0 = 32 - to.step;
+        // full chunks: runs -> the warp's tile [owned column][4] -> one tensor-map store per warp
+        const bool tst = to.tstore != 0 && nrw == RW;
+        const int wts = (g.tau * to.step * 4 + 31) & ~31;  // floats per warp tile (128-byte multiple)
+        float* wt = tst ? tl + wid * wts : nullptr;
         if (nrw > 0) {
             switch (g.tau) {
-                case 1: average_shfl_direct<1, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
-                case 2: average_shfl_direct<2, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
-                default: average_shfl_direct<3, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
+                case 1: average_shfl_direct<1, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0, wt); break;
+                case 2: average_shfl_direct<2, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0, wt); break;
+                default: average_shfl_direct<3, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0, wt); break;
+            }
+        }
+        if (tst) {
+            fence_proxy_async_shared();  // the lanes' tile writes before the async-proxy read
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&tmO, y0 * C, xa + g.tau * own0, wt);
+                bulk_commit_and_wait_read();
             }
         }
         return;
@@ -2467,17 +2499,30 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
                  encode_rows_map(&tmG, pl.guid, (long long)g.Wl * CG, (long long)g.batch * g.Hl, PGh, NW * RW + 1))
                     ? 2
                     : 0;
+        // one tensor-map store per warp for the interior tiles' 4-float column runs (one channel,
+        // 4-row chunks, one image, transposed output on 16-byte bounds)
+        static const int tstore_env = [] {
+            // schedule knob: 1 = tensor-map stores; measured neutral on c5 (30.1k vs 30.2k MPix/s:
+            // the 16-byte-wide box gains nothing over per-lane float4 stores), so off by default
+            const char* v = std::getenv("SGWLS_KB_TSTORE");
+            return v ? std::atoi(v) : 0;
+        }();
+        CUtensorMap tmO;
+        std::memset(&tmO, 0, sizeof tmO);
+        const bool tstore = tstore_env && C == 1 && RW * C == 4 && g.batch == 1 && pl.transpose_out && !pl.ratio &&
+                            g.tau <= 3 && g.Hl % 4 == 0 &&
+                            encode_rows_map(&tmO, pl.out, (long long)g.Hl * C, g.Wl, 4, g.tau * pl.step);
         // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
         // triggering) or, with a single KA tile per band, KA itself
         const bool early = slab || PSA > 1;
         const int nwa_shift = (NWA & (NWA - 1)) == 0 ? __builtin_ctz((unsigned)NWA) : -1;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, nwa_shift, pl.ratio,
-                   pl.ratio_floor, pl.und, stage_mode};
+                   pl.ratio_floor, pl.und, stage_mode, tstore ? 1 : 0};
         const dim3 kgrid(pl.ncta, PB, g.batch);
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         e = launch_pdl(kb_tile<R, C, CG>, kgrid, dim3(32, NW), smem, st, g, pl.src, pl.guid, (const float*)pl.z,
-                       (const float*)pl.maps, to, pl.err, *pl.w, tmF, tmG);
+                       (const float*)pl.maps, to, pl.err, *pl.w, tmF, tmG, tmO);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
