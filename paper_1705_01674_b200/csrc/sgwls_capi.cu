@@ -11,6 +11,7 @@
 // no float atomics).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -455,6 +456,14 @@ void sparse_fusable(int batch, int W, int H, int C, int Cg, const sgwls_b200_con
     ratio = (((fa + T - 1) & 1) == 0 ? ap0 : ap1).fast;
 }
 
+// interpolate_sparse of a host batch through the host pipeline.  Field validation of every
+// sub-batch is enqueued with it (no host synchronisation in flight); the statuses are read once
+// at the end and the first failing pair in batch order decides the error, as the reference's
+// per-call checks would (proj/src/smoother.cpp:129-144), before any pivot failure of that pair's
+// sub-batch.  On an error the output buffers hold unspecified values.
+void sparse_host_pipelined(const float* v, const float* m, const float* g, int batch, int sub, int width, int height,
+                           int channels, int gch, const sgwls_b200_config* cfg, float* out, float* und);
+
 std::string pivot_message(unsigned long long key) {
     const unsigned k0 = (unsigned)(key & 0xffffffffu);
     return "rband_lu_factorize: non-positive pivot at row " + std::to_string(k0) + " (input not SPD)";
@@ -542,20 +551,190 @@ void finish_sync(unsigned long long* d_err, cudaStream_t st) {
 
 
 // host buffers -> device -> T passes -> host, on the calling thread's stream
+// Host-buffer batches run as a three-stage pipeline over sub-batches: the upload of
+// sub-batch i+1, the filter of sub-batch i and the download of sub-batch i-1 proceed on
+// three streams (PCIe is full duplex; from pinned buffers the copies are truly
+// asynchronous), two buffer slots.  `upload(i0, n, slot, st)`, `compute(i0, n, slot, st)`,
+// `download(i0, n, slot, st)` enqueue the stage of images [i0, i0 + n) on the given stream.
+struct HostPipeline {
+    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> ev;
+    HostPipeline() {
+        CK(cudaStreamCreateWithFlags(&s_in, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s_cmp, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&s_out, cudaStreamNonBlocking));
+    }
+    ~HostPipeline() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+        if (s_in) cudaStreamDestroy(s_in);
+        if (s_cmp) cudaStreamDestroy(s_cmp);
+        if (s_out) cudaStreamDestroy(s_out);
+    }
+    cudaEvent_t event() {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        ev.push_back(e);
+        return e;
+    }
+    template <class U, class F, class D>
+    void run(int batch, int sub, U&& upload, F&& compute, D&& download) {
+        const int nsub = (batch + sub - 1) / sub;
+        std::vector<cudaEvent_t> in_done(nsub), cmp_done(nsub), out_done(nsub);
+        for (int i = 0; i < nsub; ++i) {
+            const int i0 = i * sub, n = std::min(sub, batch - i0), slot = i & 1;
+            in_done[i] = event();
+            cmp_done[i] = event();
+            out_done[i] = event();
+            if (i >= 2) CK(cudaStreamWaitEvent(s_in, cmp_done[i - 2], 0));  // the slot's inputs were consumed
+            upload(i0, n, slot, s_in);
+            CK(cudaEventRecord(in_done[i], s_in));
+            CK(cudaStreamWaitEvent(s_cmp, in_done[i], 0));
+            if (i >= 2) CK(cudaStreamWaitEvent(s_cmp, out_done[i - 2], 0));  // the slot's outputs were read
+            compute(i0, n, slot, s_cmp);
+            CK(cudaEventRecord(cmp_done[i], s_cmp));
+            CK(cudaStreamWaitEvent(s_out, cmp_done[i], 0));
+            download(i0, n, slot, s_out);
+            CK(cudaEventRecord(out_done[i], s_out));
+        }
+        CK(cudaStreamSynchronize(s_in));
+        CK(cudaStreamSynchronize(s_cmp));
+        CK(cudaStreamSynchronize(s_out));
+    }
+};
+
+// images per sub-batch of the host pipeline: ~8 stages, at least ~4 MPix each (the filter's
+// launches stay wide), one stage for small batches
+int pipeline_sub(int batch, long long px_per_image) {
+    if (batch < 4) return batch;
+    long long sub = (batch + 7) / 8;
+    const long long min_imgs = (4LL << 20) / (px_per_image > 0 ? px_per_image : 1) + 1;
+    if (sub < min_imgs) sub = min_imgs;
+    return sub >= batch ? batch : (int)sub;
+}
+
 void smooth_host(const float* t, const float* g, int batch, int width, int height, int channels, int gch,
                  const sgwls_b200_config* cfg, float* out) {
-    cudaStream_t st = cudaStreamPerThread;
-    const size_t nt = (size_t)batch * width * height * channels, ng = (size_t)batch * width * height * gch;
-    DevBuf dt, dg, dout;
-    dt.alloc(nt, st);
-    dg.alloc(ng, st);
-    dout.alloc(nt, st);
-    CK(cudaMemcpyAsync(dt.p, t, nt * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(dg.p, g, ng * 4, cudaMemcpyHostToDevice, st));
-    ErrWord ew(st);
-    run_smooth(dt.p, dg.p, batch, width, height, channels, gch, cfg, dout.p, ew.d, st);
-    CK(cudaMemcpyAsync(out, dout.p, nt * 4, cudaMemcpyDeviceToHost, st));
-    finish_sync(ew.d, st);
+    const size_t it = (size_t)width * height * channels, ig = (size_t)width * height * gch;
+    // self-guided call (sgwls::smooth(img, img, cfg), e.g. proj/src/apps.cpp:59): one upload serves both
+    const bool same = (g == t) && gch == channels;
+    const int sub = pipeline_sub(batch, (long long)width * height);
+    if (sub >= batch) {
+        cudaStream_t st = cudaStreamPerThread;
+        DevBuf dt, dg, dout;
+        dt.alloc(it * batch, st);
+        if (!same) dg.alloc(ig * batch, st);
+        dout.alloc(it * batch, st);
+        CK(cudaMemcpyAsync(dt.p, t, it * batch * 4, cudaMemcpyHostToDevice, st));
+        if (!same) CK(cudaMemcpyAsync(dg.p, g, ig * batch * 4, cudaMemcpyHostToDevice, st));
+        ErrWord ew(st);
+        run_smooth(dt.p, same ? dt.p : dg.p, batch, width, height, channels, gch, cfg, dout.p, ew.d, st);
+        CK(cudaMemcpyAsync(out, dout.p, it * batch * 4, cudaMemcpyDeviceToHost, st));
+        finish_sync(ew.d, st);
+        return;
+    }
+    HostPipeline hp;
+    const int nsub = (batch + sub - 1) / sub;
+    DevBuf dt[2], dg[2], dout[2];
+    for (int k = 0; k < 2; ++k) {
+        dt[k].alloc(it * sub, hp.s_in);
+        if (!same) dg[k].alloc(ig * sub, hp.s_in);
+        dout[k].alloc(it * sub, hp.s_in);
+    }
+    // one pivot-error word per sub-batch: the first failing sub-batch (batch order) reports
+    unsigned long long* d_errs = nullptr;
+    CK(cudaMallocAsync((void**)&d_errs, (size_t)nsub * sizeof(unsigned long long), hp.s_in));
+    CK(cudaMemsetAsync(d_errs, 0xff, (size_t)nsub * sizeof(unsigned long long), hp.s_in));
+    std::vector<unsigned long long> h_errs(nsub, ULLONG_MAX);
+    try {
+        hp.run(
+            batch, sub,
+            [&](int i0, int n, int k, cudaStream_t st) {
+                CK(cudaMemcpyAsync(dt[k].p, t + it * i0, it * n * 4, cudaMemcpyHostToDevice, st));
+                if (!same) CK(cudaMemcpyAsync(dg[k].p, g + ig * i0, ig * n * 4, cudaMemcpyHostToDevice, st));
+            },
+            [&](int i0, int n, int k, cudaStream_t st) {
+                run_smooth(dt[k].p, same ? dt[k].p : dg[k].p, n, width, height, channels, gch, cfg, dout[k].p,
+                           d_errs + i0 / sub, st);
+            },
+            [&](int i0, int n, int k, cudaStream_t st) {
+                CK(cudaMemcpyAsync(out + it * i0, dout[k].p, it * n * 4, cudaMemcpyDeviceToHost, st));
+            });
+        CK(cudaMemcpyAsync(h_errs.data(), d_errs, (size_t)nsub * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                           hp.s_cmp));
+        CK(cudaStreamSynchronize(hp.s_cmp));
+    } catch (...) {
+        cudaDeviceSynchronize();
+        cudaFreeAsync(d_errs, hp.s_in);
+        cudaStreamSynchronize(hp.s_in);
+        throw;
+    }
+    cudaFreeAsync(d_errs, hp.s_in);
+    // (the slots are released by their DevBufs on s_in, before hp's streams go: reverse declaration order)
+    for (unsigned long long h : h_errs)
+        if (h != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(h)};
+}
+
+void sparse_host_pipelined(const float* v, const float* m, const float* g, int batch, int sub, int width, int height,
+                           int channels, int gch, const sgwls_b200_config* cfg, float* out, float* und) {
+    const size_t ipx = (size_t)width * height;
+    const int nsub = (batch + sub - 1) / sub;
+    HostPipeline hp;
+    DevBuf dv[2], dm[2], dg[2], dout[2], dund[2];
+    for (int k = 0; k < 2; ++k) {
+        dv[k].alloc(ipx * channels * sub, hp.s_in);
+        dm[k].alloc(ipx * sub, hp.s_in);
+        dg[k].alloc(ipx * gch * sub, hp.s_in);
+        dout[k].alloc(ipx * channels * sub, hp.s_in);
+        if (und) dund[k].alloc(ipx * sub, hp.s_in);
+    }
+    // per pair: [first offending pixel | mask non-empty]; per sub-batch: the pivot word
+    unsigned long long* d_stat = nullptr;
+    const size_t nstat = 2 * (size_t)batch + nsub;
+    CK(cudaMallocAsync((void**)&d_stat, nstat * sizeof(unsigned long long), hp.s_in));
+    CK(cudaMemsetAsync(d_stat, 0xff, nstat * sizeof(unsigned long long), hp.s_in));
+    std::vector<unsigned long long> h(nstat);
+    try {
+        hp.run(
+            batch, sub,
+            [&](int i0, int n, int k, cudaStream_t st) {
+                CK(cudaMemcpyAsync(dv[k].p, v + ipx * channels * i0, ipx * channels * n * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(dm[k].p, m + ipx * i0, ipx * n * 4, cudaMemcpyHostToDevice, st));
+                CK(cudaMemcpyAsync(dg[k].p, g + ipx * gch * i0, ipx * gch * n * 4, cudaMemcpyHostToDevice, st));
+            },
+            [&](int i0, int n, int k, cudaStream_t st) {
+                // status layout of launch_validate_sparse for this sub-batch: [n minima][n non-empty flags]
+                unsigned long long* stat = d_stat + 2 * (size_t)i0;
+                CK(cudaMemsetAsync(stat + n, 0, (size_t)n * sizeof(unsigned long long), st));
+                CK(launch_validate_sparse(dv[k].p, dm[k].p, (long long)ipx, channels, n, stat, st));
+                run_sparse(dv[k].p, dm[k].p, dg[k].p, n, width, height, channels, gch, cfg, dout[k].p, dund[k].p,
+                           d_stat + 2 * (size_t)batch + i0 / sub, st);
+            },
+            [&](int i0, int n, int k, cudaStream_t st) {
+                CK(cudaMemcpyAsync(out + ipx * channels * i0, dout[k].p, ipx * channels * n * 4, cudaMemcpyDeviceToHost, st));
+                if (und) CK(cudaMemcpyAsync(und + ipx * i0, dund[k].p, ipx * n * 4, cudaMemcpyDeviceToHost, st));
+            });
+        CK(cudaMemcpyAsync(h.data(), d_stat, nstat * sizeof(unsigned long long), cudaMemcpyDeviceToHost, hp.s_cmp));
+        CK(cudaStreamSynchronize(hp.s_cmp));
+    } catch (...) {
+        cudaDeviceSynchronize();
+        cudaFreeAsync(d_stat, hp.s_in);
+        throw;
+    }
+    cudaFreeAsync(d_stat, hp.s_in);
+    for (int i = 0; i < nsub; ++i) {
+        const int i0 = i * sub, n = std::min(sub, batch - i0);
+        for (int b = 0; b < n; ++b) {
+            const unsigned long long bad = h[2 * (size_t)i0 + b], any = h[2 * (size_t)i0 + n + b];
+            if (bad != ULLONG_MAX) {
+                const float mv = m[ipx * (i0 + b) + bad];  // which violation: the host mask tells
+                if (mv != 0.f && mv != 1.f) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: mask must be 0/1"};
+                throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: values nonzero outside mask"};
+            }
+            if (any == 0) throw Fail{SGWLS_B200_EINVAL, "interpolate_sparse: empty mask"};
+        }
+        const unsigned long long piv = h[2 * (size_t)batch + i];
+        if (piv != ULLONG_MAX) throw Fail{SGWLS_B200_EINVAL, pivot_message(piv)};
+    }
 }
 
 // ------------------------------------------------------ CUDA-graph replay
@@ -899,6 +1078,12 @@ int sgwls_b200_interpolate_sparse_batch(const float* v, const float* m, const fl
         int rc = check_shape(batch, width, height, channels + 1, gch, msg);
         if (rc) throw Fail{rc, msg};
         require_device();
+        const int sub = pipeline_sub(batch, (long long)width * height);
+        rc = validate_cfg(cfg, msg);
+        if (sub < batch && rc == 0) {  // three-stage pipeline over sub-batches (valid configuration)
+            sparse_host_pipelined(v, m, g, batch, sub, width, height, channels, gch, cfg, out, und);
+            return;
+        }
         cudaStream_t st = cudaStreamPerThread;
         const size_t npx = (size_t)batch * width * height;
         DevBuf dv, dm, dg, dout, dund;
@@ -912,7 +1097,6 @@ int sgwls_b200_interpolate_sparse_batch(const float* v, const float* m, const fl
         CK(cudaMemcpyAsync(dg.p, g, npx * gch * 4, cudaMemcpyHostToDevice, st));
         // the reference validates the field before the configuration (smooth() validates cfg)
         validate_sparse(dv.p, dm.p, batch, (long long)width * height, channels, st);
-        rc = validate_cfg(cfg, msg);
         if (rc) throw Fail{rc, msg};
         ErrWord ew(st);
         run_sparse(dv.p, dm.p, dg.p, batch, width, height, channels, gch, cfg, dout.p, dund.p, ew.d, st);

@@ -140,12 +140,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* mbar, unsigned par
         "{\n"
         ".reg .pred p;\n"
         "MBAR_WAIT:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@p bra MBAR_DONE;\n"
         "bra MBAR_WAIT;\n"
         "MBAR_DONE:\n"
         "}" ::"r"((unsigned)__cvta_generic_to_shared(mbar)),
-        "r"(parity)
+        "r"(parity), "r"(0x989680u)  // suspend-time hint: the warp sleeps in the barrier instead of polling
         : "memory");
 }
 

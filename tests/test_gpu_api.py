@@ -99,3 +99,72 @@ def test_graph_cache_is_bounded():
         assert torch.equal(o, ref)
     n = S.graph_clear()
     assert n == S.graph_count() + n and S.graph_count() == 0
+
+
+# ------------------------------------------------ host batches: pipeline + aliasing
+
+def _scene(h, w, seed):
+    rng = np.random.default_rng(seed)
+    y, x = np.mgrid[0:h, 0:w]
+    g = (0.2 + 0.25 * ((x // 97 + y // 61) % 3) + rng.normal(0, 0.02, (h, w))).astype(np.float32)
+    return np.clip(g, 0, 1)
+
+
+def test_self_guided_call_uploads_once_same_result():
+    """smooth(img, img, cfg) (proj/src/apps.cpp:59): one host buffer for target and guidance
+    is uploaded once; the result is bit-identical to two separate buffers"""
+    t = _scene(300, 260, 1)
+    cfg = S.SmoothConfig(lambda_=400.0, r=2, tau=3, weight=S.WeightParams(kind=S.WeightKind.Exp, sigma_r=0.05))
+    a = S.smooth(t, t, cfg)
+    b = S.smooth(t, t.copy(), cfg)
+    assert np.array_equal(a, b)
+
+
+def test_host_batch_pipeline_equals_single_calls():
+    """Host batches beyond ~8 MPix run as upload / filter / download stages over sub-batches
+    (6 images of 1 MPix: sub-batches of 5 + 1): bit-identical to the single calls"""
+    cfg = S.SmoothConfig(lambda_=400.0, r=2, tau=2, weight=S.WeightParams(kind=S.WeightKind.Exp, sigma_r=0.05))
+    t = np.stack([_scene(1024, 1024, 10 + i) for i in range(6)])
+    g = np.stack([_scene(1024, 1024, 20 + i) for i in range(6)])
+    got = S.smooth_batch(t, g, cfg)
+    for i in (0, 4, 5):
+        assert np.array_equal(got[i], S.smooth(t[i], g[i], cfg)), i
+    # sparse: values / mask / guidance triples, the undefined mask too
+    rng = np.random.default_rng(5)
+    m = (rng.uniform(size=t.shape) < 1 / 16).astype(np.float32)
+    v = (t * m).astype(np.float32)
+    out, und = S.interpolate_sparse_batch(v, m, g, cfg)
+    for i in (0, 5):
+        o1, u1 = S.interpolate_sparse(S.SparseField(v[i], m[i]), g[i], cfg, return_undefined=True)
+        assert np.array_equal(out[i], o1.reshape(out[i].shape)) and np.array_equal(und[i], u1.reshape(und[i].shape)), i
+
+
+def test_host_batch_pipeline_reports_first_failing_pair():
+    """Errors of a pipelined batch: the first failing pair in batch order decides, field
+    checks before the pivot failure of the same sub-batch (proj/src/smoother.cpp:129-144)"""
+    cfg = S.SmoothConfig(lambda_=400.0, r=2, tau=2, weight=S.WeightParams(kind=S.WeightKind.Exp, sigma_r=0.05))
+    g = np.stack([_scene(1024, 1024, 30 + i) for i in range(6)])
+    rng = np.random.default_rng(6)
+    m = (rng.uniform(size=g.shape) < 1 / 16).astype(np.float32)
+    v = (g * m).astype(np.float32)
+    m2, v2 = m.copy(), v.copy()
+    m2[5] = 0.0
+    v2[5] = 0.0                                   # pair 5: empty mask
+    with pytest.raises(S.Error, match="interpolate_sparse: empty mask"):
+        S.interpolate_sparse_batch(v2, m2, g, cfg)
+    m2[3, 17, 19] = 0.5                           # pair 3: not 0/1 -> decides before pair 5
+    with pytest.raises(S.Error, match="interpolate_sparse: mask must be 0/1"):
+        S.interpolate_sparse_batch(v2, m2, g, cfg)
+    v3 = v.copy()
+    v3[5, 100, 100] = 0.25 if m[5, 100, 100] == 0 else v3[5, 100, 100]
+    m3 = m.copy()
+    m3[5, 100, 100] = 0.0
+    v3[5, 100, 100] = 0.25                        # value outside the mask, second sub-batch
+    with pytest.raises(S.Error, match="interpolate_sparse: values nonzero outside mask"):
+        S.interpolate_sparse_batch(v3, m3, g, cfg)
+    gb = g.copy()
+    gb[5, 300, 400] = np.nan                      # NaN guidance: the reference's pivot failure
+    with pytest.raises(S.Error, match="non-positive pivot"):
+        S.interpolate_sparse_batch(v, m, gb, cfg)
+    with pytest.raises(S.Error, match="non-positive pivot"):
+        S.smooth_batch(v, gb, cfg)
