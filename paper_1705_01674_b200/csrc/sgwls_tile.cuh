@@ -1649,6 +1649,9 @@ struct TileOut {
     int stage;
     // interior tiles send each warp's owned 4-float column runs with one tensor-map store
     int tstore;
+    // band tiles [lean_lo, lean_hi) run kb_lean (host: the launch-uniform conditions hold and the
+    // tile is interior); empty range otherwise
+    int lean_lo, lean_hi;
 };
 
 // 1/n correctly rounded (what 1.0f / n gives) for the band count of a column, n <= 2r + 2 <= 10
@@ -1835,6 +1838,152 @@ __device__ __forceinline__ void apply_map(const float* ms, const float (&zA)[R][
         }
 }
 
+// The lean body is compiled into the instantiations that can use it by default (r = 2, one
+// channel: staged by tensor maps, 4-float runs); carrying it elsewhere only grows the kernel
+// (measured: c3's r = 3 KB -14 %, c4's two-channel KB -3 % with the unused body inside)
+__host__ __device__ constexpr bool kb_has_lean(int R, int C) { return R == 2 && C == 1; }
+
+// Lean body of kb_tile for INTERIOR band tiles of the common launch: tensor-map staged
+// input, shuffle averaging with direct transposed stores, no row-slab neighbours, no fused
+// ratio.  Everything launch-uniform was decided on the host (to.lean_lo / lean_hi), every band
+// of the tile is regular (lo = tau*b, all 32 lanes active, compile-time band counts), so the
+// general kernel's tile-layout, ownership-table and predicate set-up is not executed at all.
+// Same device functions as the general path: bit-identical results.
+template <int R, int C, int CG>
+__device__ __forceinline__ void kb_lean(const PassGeom& g, const float* __restrict__ zsep,
+                                        const float* __restrict__ maps, const TileOut& to,
+                                        unsigned long long* __restrict__ err, const WeightDev& W,
+                                        const CUtensorMap* tmF, const CUtensorMap* tmG, float* sm) {
+    constexpr int RW = rows_per_chunk(R, C);
+    constexpr int M = 2 * R + 1, K = RW * M;
+    constexpr int DVEC = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
+    using RL = Rec<R, C>;
+    const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
+    const int tid = wid * 32 + lane;
+    const int tau = g.tau;
+    const int B0 = blockIdx.x * to.step, J = blockIdx.y, img = blockIdx.z;
+    const int j = J * NW + wid, y0 = j * RW, Y0 = J * NW * RW;
+    const int nw = min(NW, g.P - J * NW);
+    const int xa = tau * B0;
+    const long long NLl = (long long)g.nb * g.batch;
+    const long long L0 = (long long)img * g.nb + B0;
+    // shared memory: [maps: warp x slot x lane x MAPP][mbarriers, 128 B][image rows][guidance rows]
+    const int PF = kb_stage_pitch(tau, M, C), PG = kb_stage_pitch(tau, M, CG);
+    float* mapw = sm + wid * 2 * 32 * RL::MAPP;
+    unsigned long long* mbar = reinterpret_cast<unsigned long long*>(sm + NW * 2 * 32 * RL::MAPP);
+    unsigned long long* mbar_w = mbar + 1 + wid;
+    float* sF = sm + NW * 2 * 32 * RL::MAPP + 32;
+    float* sG = sF + ((NW * RW * PF + 31) & ~31);
+    const int xoF = (xa * C) & 3, xoG = (xa * CG) & 3;
+    if (tid <= NW) mbar_init(mbar + tid, 1);
+    __syncthreads();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(mbar, (unsigned)((NW * RW * PF + (NW * RW + 1) * PG) * sizeof(float)));
+        tma_load_2d(sF, tmF, xa * C - xoF, img * g.Hl + Y0, mbar);
+        tma_load_2d(sG, tmG, xa * CG - xoG, img * g.Hl + Y0 - 1, mbar);
+    }
+    if (wid >= nw) return;  // chunk rows past the image: nothing else synchronises the CTA
+    const int JA = to.nwa_shift >= 0 ? j >> to.nwa_shift : j / to.nwa, sj = j - JA * to.nwa;
+    const bool lastc = j == g.P - 1, has_left = j > 0;
+    const bool r_inner = !lastc && sj < to.nwa - 1, l_inner = sj > 0;
+    auto fetch_maps = [&]() {
+        if (lane == 0 && (l_inner || r_inner)) {
+            const unsigned by = (unsigned)(32 * RL::MAPP * sizeof(float));
+            const float* gp0 = maps + ((long long)j * NLl + L0) * RL::MAPP;
+            mbar_arrive_expect_tx(mbar_w, by * ((l_inner ? 1 : 0) + (r_inner ? 1 : 0)));
+            if (l_inner) bulk_g2s(mapw, gp0 - NLl * RL::MAPP, by, mbar_w);
+            if (r_inner) bulk_g2s(mapw + 32 * RL::MAPP, gp0, by, mbar_w);
+        }
+    };
+    if (to.early) fetch_maps();
+    const int nrows = min(RW, g.Hl - y0);
+    ChunkInL<R, C, CG, RW> in;
+    mbar_wait(mbar, 0);
+    {
+        const float* sFr = sF + (y0 - Y0) * PF + xoF + tau * lane * C;
+        const float* sGr = sG + (y0 - Y0 + 1) * PG + xoG + tau * lane * CG;
+        if (nrows == RW)
+            load_chunk_lazy_staged<R, C, CG, RW, true>(in, sFr, PF, sGr, PG, g, y0, nrows);
+        else
+            load_chunk_lazy_staged<R, C, CG, RW, false>(in, sFr, PF, sGr, PG, g, y0, nrows);
+    }
+    const long long L = L0 + lane;
+    if (err != nullptr) {  // NaN guidance: the reference's pivot failure (rare path locates it)
+        float acc = 0.f;
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int c = 0; c < CG; ++c) acc = fmaf(in.gp[k][c], 0.f, acc);
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+            for (int c = 0; c < CG; ++c) acc = fmaf(in.gprev[i][c], 0.f, acc);
+        if (!(acc >= 0.f)) {
+            const LazyWeights<R, C, CG, RW, 1> we{in, W};
+            const LazyWeights<R, C, CG, RW, 0> wf{in, W};
+            int bad = 0x7fffffff;
+#pragma unroll
+            for (int k = 0; k < K; ++k)
+#pragma unroll
+                for (int t = 1; t <= R; ++t) {
+                    const float lw = W.kind == 1 ? we(k, t) : wf(k, t);
+                    const bool exists = (k / M < nrows) && (k - t >= 0 || y0 > 0);
+                    bad = (!(lw >= 0.f) && exists) ? min(bad, (g.row0 + y0) * M + k - t) : bad;
+                }
+            if (bad != 0x7fffffff) atomicMin(err, ((unsigned long long)(unsigned)L << 32) | (unsigned)bad);
+        }
+    }
+    pdl_wait();  // super-separators (K2), maps (KA)
+    pdl_trigger();
+    if (!to.early) fetch_maps();
+    float zl[R][C], zr[R][C];
+    {
+        const bool hA = JA > 0, hB = JA < to.psa - 1;
+        const float* zb = zsep + (long long)JA * R * C * NLl + L;
+        float zA[R][C], zB[R][C];
+#pragma unroll
+        for (int q = 0; q < R; ++q)
+#pragma unroll
+            for (int c = 0; c < C; ++c) {
+                zA[q][c] = hA ? zb[((long long)(q - R) * C + c) * NLl] : 0.f;
+                zB[q][c] = hB ? zb[(q * C + c) * NLl] : 0.f;
+                zl[q][c] = has_left ? zA[q][c] : 0.f;
+                zr[q][c] = lastc ? 0.f : zB[q][c];
+            }
+        if (l_inner || r_inner) mbar_wait(mbar_w, 0);
+        if (r_inner) apply_map<R, C>(mapw + (32 + lane) * RL::MAPP, zA, zB, zr);
+        if (l_inner) apply_map<R, C>(mapw + lane * RL::MAPP, zA, zB, zl);
+    }
+    const int kv = nrows * M;
+    const int kend = lastc ? kv : kv - R;
+    float cs[K][R], ys[K][C];
+#pragma unroll
+    for (int p = 0; p < K; ++p) {
+#pragma unroll
+        for (int i = 0; i < R; ++i) cs[p][i] = 0.f;
+#pragma unroll
+        for (int c = 0; c < C; ++c) ys[p][c] = 0.f;
+    }
+    auto solve = [&](const auto& lwf) {
+        if (!lastc && kv == K)
+            chunk_interior_solve<R, C, CG, RW, true>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
+        else
+            chunk_interior_solve<R, C, CG, RW, false>(in, lwf, has_left, lastc, kv, kend, zl, zr, cs, ys);
+    };
+    if (W.kind == 1)
+        solve(LazyWeights<R, C, CG, RW, 1>{in, W});
+    else
+        solve(LazyWeights<R, C, CG, RW, 0>{in, W});
+    float* obase = to.out + img * g.img_stride + ((long long)xa * g.Hl + y0) * C;
+    const long long opitch = (long long)g.Hl * C;
+    const int own0 = 32 - to.step, par0 = y0 & 1;
+    switch (tau) {
+        case 1: average_shfl_direct<1, R, C, K, DVEC, true>(ys, nrows, par0, lane, obase, opitch, 0, nullptr, own0); break;
+        case 2: average_shfl_direct<2, R, C, K, DVEC, true>(ys, nrows, par0, lane, obase, opitch, 0, nullptr, own0); break;
+        default: average_shfl_direct<3, R, C, K, DVEC, true>(ys, nrows, par0, lane, obase, opitch, 0, nullptr, own0); break;
+    }
+}
+
 template <int R, int C, int CG>
 __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restrict__ src,
                                                const float* __restrict__ guid, const float* __restrict__ zsep,
@@ -1847,6 +1996,12 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1, K = RW * M;
     extern __shared__ __align__(128) float sm[];
+    if constexpr (kb_has_lean(R, C)) {
+        if ((int)blockIdx.x >= to.lean_lo && (int)blockIdx.x < to.lean_hi) {  // interior band tiles of a lean launch
+            kb_lean<R, C, CG>(g, zsep, maps, to, err, W, &tmF, &tmG, sm);
+            return;
+        }
+    }
     const int lane = threadIdx.x, wid = threadIdx.y, NW = blockDim.y;
     const int tid = wid * 32 + lane, NT = NW * 32;
     // grid: (band tile, chunk tile, image)
@@ -2517,7 +2672,38 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         const bool early = slab || PSA > 1;
         const int nwa_shift = (NWA & (NWA - 1)) == 0 ? __builtin_ctz((unsigned)NWA) : -1;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, nwa_shift, pl.ratio,
-                   pl.ratio_floor, pl.und, stage_mode, tstore ? 1 : 0};
+                   pl.ratio_floor, pl.und, stage_mode, tstore ? 1 : 0, 0, 0};
+        {
+            // lean launch: staged by tensor maps, overlapping bands averaged by shuffles and stored
+            // directly (the conditions of kb_tile's `direct`, all launch-uniform here), several chunks
+            static const int lean_env = [] {
+                const char* v = std::getenv("SGWLS_KB_LEAN");  // schedule knob: 0 = general body everywhere
+                return v ? std::atoi(v) : 1;
+            }();
+            constexpr int DV = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
+            const bool lean_ok = kb_has_lean(R, C) && lean_env && stage_mode == 2 && !tstore && g.P > 1 && pl.nph > 1 && g.tau <= 3 &&
+                                 !pl.ratio && pl.transpose_out && (C == 1 || DV == 4) &&
+                                 ((long long)g.Hl * C) % DV == 0 && (g.img_stride % DV) == 0 &&
+                                 (reinterpret_cast<uintptr_t>(pl.out) & (DV * 4 - 1)) == 0;
+            if (lean_ok) {
+                int lo_bx = -1, hi_bx = -1;
+                for (int bx = 0; bx < pl.ncta; ++bx) {
+                    const int B0 = bx * pl.step;
+                    const bool interior = bx > 0 && B0 + 32 < g.nb && B0 + 32 <= g.nreg &&
+                                          (long long)(B0 + 32) * g.tau <= g.Wl - 1 - 2 * g.r;
+                    if (interior) {
+                        if (lo_bx < 0) lo_bx = bx;
+                        hi_bx = bx + 1;
+                    } else if (lo_bx >= 0) {
+                        break;
+                    }
+                }
+                if (lo_bx >= 0) {
+                    to.lean_lo = lo_bx;
+                    to.lean_hi = hi_bx;
+                }
+            }
+        }
         const dim3 kgrid(pl.ncta, PB, g.batch);
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
