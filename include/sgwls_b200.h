@@ -76,11 +76,14 @@ void sgwls_b200_config_default(sgwls_b200_config* cfg);
 /* SmoothConfig::validate (proj/src/smoother.cpp:103-111) incl. WeightParams::validate. */
 int sgwls_b200_validate(const sgwls_b200_config* cfg, char* err, size_t errlen);
 
-/* sgwls::smooth on host buffers (synchronous).  out: width*height*channels floats. */
+/* sgwls::smooth on host buffers (synchronous).  out: width*height*channels floats.  A self-guided
+ * call (guidance == target, same channel count; proj/src/apps.cpp:59) uploads the buffer once. */
 int sgwls_b200_smooth(const float* target, int width, int height, int channels, const float* guidance,
                       int guidance_channels, const sgwls_b200_config* cfg, float* out, char* err, size_t errlen);
 
-/* `batch` independent smooth calls (target i with guidance i) in one launch sequence. */
+/* `batch` independent smooth calls (target i with guidance i).  Batches above ~8 MPix run as an
+ * upload / filter / download pipeline over sub-batches on three streams (fastest from pinned
+ * host buffers); results and errors as `batch` serial calls (the first failing image decides). */
 int sgwls_b200_smooth_batch(const float* targets, const float* guidances, int batch, int width, int height,
                             int channels, int guidance_channels, const sgwls_b200_config* cfg, float* out,
                             char* err, size_t errlen);
@@ -139,6 +142,10 @@ int sgwls_b200_profile_read(char* json, size_t len);
  * call after every replay when profiling graph-replayed calls. */
 void sgwls_b200_profile_collect(void);
 
+/* out[b][x][y][c] = in[b][y][x][c] on device buffers (width x height -> height x width), stream-ordered */
+int sgwls_b200_transpose_device(const float* d_in, float* d_out, int batch, int width, int height, int channels,
+                                void* stream, char* err, size_t errlen);
+
 /* ---- row-slab mode: one Column pass of an image split into row slabs ----
  * (one slab per GPU; paper_1705_01674_b200/sharded.py).  The
  * band solves are partitioned exactly across slabs: phase A computes each
@@ -150,10 +157,7 @@ void sgwls_b200_profile_collect(void);
  * with row -1 (the previous slab's last row) readable when islab > 0; d_work:
  * work_floats floats kept between the phases; d_out: rows x width x channels
  * (caller layout, not transposed).  row0 (global row of the slab's first row)
- * must be even.  NaN guidance is not reported in this mode. */
-/* out[b][x][y][c] = in[b][y][x][c] on device buffers (width x height -> height x width), stream-ordered */
-int sgwls_b200_transpose_device(const float* d_in, float* d_out, int batch, int width, int height, int channels,
-                                void* stream, char* err, size_t errlen);
+ * must be even.  NaN guidance: see d_pivot_err of phase B below. */
 int sgwls_b200_slab_sizes(int width, int rows, int channels, int guidance_channels, int nslabs,
                           const sgwls_b200_config* cfg, size_t* work_floats, size_t* record_floats, char* err,
                           size_t errlen);

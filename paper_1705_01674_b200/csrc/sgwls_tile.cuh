@@ -2084,10 +2084,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                 if (a + len > end) len = end - a;
                 return (unsigned)(len * 4);
             };
-            long long aF0, aG0;
-            const unsigned bF = seg(eF + (long long)Y0 * g.Wl * C, xoF, ncol * C, endF, aF0);
-            const unsigned bG = seg(eG + (long long)Y0 * g.Wl * CG, xoG, ncol * CG, endG, aG0);
-            // the clamp can only bite in the image's very last row: count it exactly
+            // the clamp can only bite in the image's very last row: count the bytes exactly
             unsigned total = 0;
             for (int i = lane; i < nrF + nrG; i += 32) {
                 const bool isF = i < nrF;
@@ -2113,10 +2110,6 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                     bulk_g2s(sG + (rrow + 1) * PG, guid + a, by, mbar);
                 }
             }
-            (void)bF;
-            (void)bG;
-            (void)aF0;
-            (void)aG0;
         }
     }
     // ---- 1. chunk inputs and edge weights before the dependent-launch wait:
@@ -2137,8 +2130,9 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     // vector width divides the output rows
     constexpr int DVEC = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
 #ifndef SGWLS_NO_DIRECT
-    // measured on B200: c1 +8.5 %, c3 +1.8 %, c5 +0.6 %; c4 (2 channels, float2 runs) -4.7 %, so
-    // only for one channel or full float4 runs
+    // measured on B200: c1 +8.5 %, c3 +1.8 %, c5 +0.6 %; c4 (2 channels, float2 runs) -4.7 % (+0.5 %
+    // once its rows were TMA-staged: still not worth a second code path), so only for one channel
+    // or full float4 runs
     const bool direct = shfl_avg && !to.ratio && to.transpose_out && (C == 1 || DVEC == 4) &&
                         ((long long)g.Hl * C) % DVEC == 0 &&
                         (reinterpret_cast<uintptr_t>(oi) & (DVEC * 4 - 1)) == 0;
