@@ -88,14 +88,6 @@ __device__ __forceinline__ void tma_load_2d(float* sdst, const CUtensorMap* tm, 
         : "memory");
 }
 
-// Tiled TMA store of a dense shared-memory box to (x, y) of the tensor; elements past the
-// tensor's bounds are dropped.  Bulk-group completion (bulk_commit_and_wait_read).
-__device__ __forceinline__ void tma_store_2d(const CUtensorMap* tm, int x, int y, const float* ssrc) {
-    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(tm), "r"(x),
-                 "r"(y), "r"((unsigned)__cvta_generic_to_shared(ssrc))
-                 : "memory");
-}
-
 // Tensor map over `rows` rows of `row_elems` fp32 each (row pitch = row_elems), box
 // box_w x box_h, no swizzle, zero fill.  False when the driver entry point is missing
 // or the layout is outside TMA's rules (16-byte base and pitch, box sides <= 256).
@@ -1556,9 +1548,7 @@ __device__ __forceinline__ void average_shfl(const float (&ys)[K][C], int nrw, i
 template <int TAU, int R, int C, int K, int VEC, bool INTERIOR = false>
 __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int nrw, int par0, int lane,
                                                     float* obase, long long opitch, int ncol,
-                                                    const float* inv_col, int own0 = 0, float* wtile = nullptr) {
-    // wtile (INTERIOR, full chunk, 4-float runs): the owned columns' runs go to the warp's
-    // shared tile [column][4] (conflict-free 16-byte stores) for ONE tensor-map store by the caller
+                                                    const float* inv_col, int own0 = 0) {
     constexpr int M = 2 * R + 1, RW = K / M;
     constexpr int KMAX = (M - 1) / TAU;
     float acc[TAU][RW * C];
@@ -1592,13 +1582,6 @@ __device__ __forceinline__ void average_shfl_direct(const float (&ys)[K][C], int
         float sc;
         if constexpr (INTERIOR) {
             sc = 1.0f / (float)(1 + (2 * R - j) / TAU);  // compile-time, correctly rounded like kInvCount
-            if constexpr (RW * C == 4) {
-                if (wtile != nullptr) {
-                    *reinterpret_cast<float4*>(wtile + (TAU * (lane - own0) + j) * 4) =
-                        make_float4(acc[j][0] * sc, acc[j][1] * sc, acc[j][2] * sc, acc[j][3] * sc);
-                    continue;
-                }
-            }
         } else {
             if (xl >= ncol) continue;
             sc = inv_col[xl];
@@ -1647,8 +1630,6 @@ struct TileOut {
     // (TMA) copy per row segment instead of per-lane loads (r >= 2, packed input,
     // no row-slab neighbours, 16-byte aligned rows; decided on the host)
     int stage;
-    // interior tiles send each warp's owned 4-float column runs with one tensor-map store
-    int tstore;
     // band tiles [lean_lo, lean_hi) run kb_lean (host: the launch-uniform conditions hold and the
     // tile is interior); empty range otherwise
     int lean_lo, lean_hi;
@@ -1991,8 +1972,7 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
                                                unsigned long long* __restrict__ err,
                                                const __grid_constant__ WeightDev W,
                                                const __grid_constant__ CUtensorMap tmF,
-                                               const __grid_constant__ CUtensorMap tmG,
-                                               const __grid_constant__ CUtensorMap tmO) {
+                                               const __grid_constant__ CUtensorMap tmG) {
     constexpr int RW = rows_per_chunk(R, C);
     constexpr int M = 2 * R + 1, K = RW * M;
     extern __shared__ __align__(128) float sm[];
@@ -2056,60 +2036,21 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
     const int sx = colmaj ? TP : C, sy = colmaj ? C : XP;  // tile strides of x and y
     const int tsize = colmaj ? ncol * TP : TR * XP;
 
-    // ---- 0b. staged input: warp 0 issues one bulk copy per image / guidance row of the
-    //          tile (segment [xa, xb] widened to 16-byte bounds; the rows of the pass
-    //          input are complete before KA began, so this precedes the dependent-launch wait)
+    // ---- 0b. staged input: two tensor-map boxes per CTA, the tile's image rows and its guidance
+    //          rows from Y0 - 1 (the rows of the pass input are complete before KA began, so this
+    //          precedes the dependent-launch wait).  A box's first element must sit on a 16-byte
+    //          boundary: it starts up to 3 floats before column xa (the pitch has that slack) and
+    //          xoF / xoG skip them; the offset is the same for every row ((Wl*C) % 4 == 0).
     int xoF = 0, xoG = 0;
     if (stage) {
-        const long long eF = ((long long)img * g.Hl * g.Wl + xa) * C, eG = ((long long)img * g.Hl * g.Wl + xa) * CG;
-        // element offset of column xa in a row is the same modulo 4 for every row ((Wl*C) % 4 == 0)
-        xoF = (int)(eF & 3);
-        xoG = (int)(eG & 3);
+        xoF = (xa * C) & 3;
+        xoG = (xa * CG) & 3;
         if (tid <= NW) mbar_init(mbar + tid, 1);  // [0]: the tile's rows; [1 + w]: warp w's separator maps
         __syncthreads();
-        if (to.stage == 2) {  // two tensor-map boxes: the tile's image rows, its guidance rows from Y0 - 1
-            // the box's first element must sit on a 16-byte boundary: start up to 3 floats early
-            // (the pitch has that slack), xoF / xoG skip them
-            if (tid == 0) {
-                mbar_arrive_expect_tx(mbar, (unsigned)((NW * RW * PF + (NW * RW + 1) * PG) * sizeof(float)));
-                tma_load_2d(sF, &tmF, xa * C - xoF, img * g.Hl + Y0, mbar);
-                tma_load_2d(sG, &tmG, xa * CG - xoG, img * g.Hl + Y0 - 1, mbar);
-            }
-        } else if (wid == 0) {
-            const int nrF = TR, nrG = TR + (Y0 > 0 ? 1 : 0);
-            const long long endF = (long long)g.batch * g.img_stride, endG = (long long)g.batch * g.gimg_stride;
-            auto seg = [&](long long e0, int xo, int cnt, long long end, long long& a) {
-                a = e0 - xo;
-                long long len = (xo + cnt + 3) & ~3;
-                if (a + len > end) len = end - a;
-                return (unsigned)(len * 4);
-            };
-            // the clamp can only bite in the image's very last row: count the bytes exactly
-            unsigned total = 0;
-            for (int i = lane; i < nrF + nrG; i += 32) {
-                const bool isF = i < nrF;
-                const int rrow = isF ? i : i - nrF - (Y0 > 0 ? 1 : 0);  // row relative to Y0 (guidance: from -1)
-                long long a;
-                const unsigned by = isF ? seg(eF + (long long)(Y0 + rrow) * g.Wl * C, xoF, ncol * C, endF, a)
-                                        : seg(eG + (long long)(Y0 + rrow) * g.Wl * CG, xoG, ncol * CG, endG, a);
-                total += by;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
-            if (lane == 0) mbar_arrive_expect_tx(mbar, total);
-            __syncwarp();
-            for (int i = lane; i < nrF + nrG; i += 32) {
-                const bool isF = i < nrF;
-                const int rrow = isF ? i : i - nrF - (Y0 > 0 ? 1 : 0);
-                long long a;
-                if (isF) {
-                    const unsigned by = seg(eF + (long long)(Y0 + rrow) * g.Wl * C, xoF, ncol * C, endF, a);
-                    bulk_g2s(sF + rrow * PF, src + a, by, mbar);
-                } else {
-                    const unsigned by = seg(eG + (long long)(Y0 + rrow) * g.Wl * CG, xoG, ncol * CG, endG, a);
-                    bulk_g2s(sG + (rrow + 1) * PG, guid + a, by, mbar);
-                }
-            }
+        if (tid == 0) {
+            mbar_arrive_expect_tx(mbar, (unsigned)((NW * RW * PF + (NW * RW + 1) * PG) * sizeof(float)));
+            tma_load_2d(sF, &tmF, xa * C - xoF, img * g.Hl + Y0, mbar);
+            tma_load_2d(sG, &tmG, xa * CG - xoG, img * g.Hl + Y0 - 1, mbar);
         }
     }
     // ---- 1. chunk inputs and edge weights before the dependent-launch wait:
@@ -2344,23 +2285,11 @@ __global__ void SGWLS_KB_BOUNDS kb_tile(const PassGeom g, const float* __restric
         float* obase = oi + ((long long)xa * g.Hl + y0) * C;
         const long long opitch = (long long)g.Hl * C;
         const int own0 = 32 - to.step;
-        // full chunks: runs -> the warp's tile [owned column][4] -> one tensor-map store per warp
-        const bool tst = to.tstore != 0 && nrw == RW;
-        const int wts = (g.tau * to.step * 4 + 31) & ~31;  // floats per warp tile (128-byte multiple)
-        float* wt = tst ? tl + wid * wts : nullptr;
         if (nrw > 0) {
             switch (g.tau) {
-                case 1: average_shfl_direct<1, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0, wt); break;
-                case 2: average_shfl_direct<2, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0, wt); break;
-                default: average_shfl_direct<3, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0, wt); break;
-            }
-        }
-        if (tst) {
-            fence_proxy_async_shared();  // the lanes' tile writes before the async-proxy read
-            __syncwarp();
-            if (lane == 0) {
-                tma_store_2d(&tmO, y0 * C, xa + g.tau * own0, wt);
-                bulk_commit_and_wait_read();
+                case 1: average_shfl_direct<1, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
+                case 2: average_shfl_direct<2, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
+                default: average_shfl_direct<3, R, C, K, DVEC, true>(ys, nrw, par0, lane, obase, opitch, ncol, nullptr, own0); break;
             }
         }
         return;
@@ -2620,15 +2549,13 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         // staged input rows (bulk copies): lazy-weight radii, packed input, no slab neighbours,
         // rows and bases on 16-byte bounds
         static const int stage_env = [] {
-            // schedule knob: 0 = per-lane loads; 1 = one bulk copy per row segment (33 per CTA:
-            // measured c5 KB +15 %, c4 +3 %, c3 +9 % SLOWER than per-lane loads); 2 = one tensor-map
-            // box per array
-            const char* v = std::getenv("SGWLS_KB_STAGE");
+            const char* v = std::getenv("SGWLS_KB_STAGE");  // schedule knob: 0 = per-lane loads, 1 = tensor-map staging
             return v ? std::atoi(v) : -1;
         }();
-        // default: tensor-map staging (mode 2) for r = 2 -- measured c5 +3.4 %, c4 +2.6 %; c3 (r = 3,
-        // 8-row tiles) -1.9 %, so r >= 3 keeps the per-lane loads
-        const int stage_sel = stage_env >= 0 ? stage_env : (R == 2 ? 2 : 0);
+        // default: tensor-map staging for r = 2 -- measured c5 +6.5 %, c4 +3.5 %; c3 (r = 3, 8-row
+        // tiles) -1.9 %, so r >= 3 keeps the per-lane loads.  (One bulk copy per row segment instead
+        // of two tensor-map boxes per CTA was 15 % SLOWER than no staging on c5: removed.)
+        const int stage_sel = stage_env >= 0 ? stage_env : (R == 2 ? 1 : 0);
         const bool stage = stage_sel && R >= SGWLS_LAZY_MIN_R && !slab && g.msk == nullptr &&
                            ((long long)g.Wl * C) % 4 == 0 && ((long long)g.Wl * CG) % 4 == 0 &&
                            (reinterpret_cast<uintptr_t>(pl.src) & 15) == 0 &&
@@ -2641,32 +2568,18 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         CUtensorMap tmF, tmG;
         std::memset(&tmF, 0, sizeof tmF);
         std::memset(&tmG, 0, sizeof tmG);
-        int stage_mode = stage ? 1 : 0;
-        if (stage && stage_sel == 2)  // no tensor map (box side > 256, no driver entry point): per-lane loads
-            stage_mode =
-                (encode_rows_map(&tmF, pl.src, (long long)g.Wl * C, (long long)g.batch * g.Hl, PFh, NW * RW) &&
-                 encode_rows_map(&tmG, pl.guid, (long long)g.Wl * CG, (long long)g.batch * g.Hl, PGh, NW * RW + 1))
-                    ? 2
-                    : 0;
-        // one tensor-map store per warp for the interior tiles' 4-float column runs (one channel,
-        // 4-row chunks, one image, transposed output on 16-byte bounds)
-        static const int tstore_env = [] {
-            // schedule knob: 1 = tensor-map stores; measured neutral on c5 (30.1k vs 30.2k MPix/s:
-            // the 16-byte-wide box gains nothing over per-lane float4 stores), so off by default
-            const char* v = std::getenv("SGWLS_KB_TSTORE");
-            return v ? std::atoi(v) : 0;
-        }();
-        CUtensorMap tmO;
-        std::memset(&tmO, 0, sizeof tmO);
-        const bool tstore = tstore_env && C == 1 && RW * C == 4 && g.batch == 1 && pl.transpose_out && !pl.ratio &&
-                            g.tau <= 3 && g.Hl % 4 == 0 &&
-                            encode_rows_map(&tmO, pl.out, (long long)g.Hl * C, g.Wl, 4, g.tau * pl.step);
+        // no tensor map (box side > 256, no driver entry point): per-lane loads
+        const int stage_mode =
+            (stage && encode_rows_map(&tmF, pl.src, (long long)g.Wl * C, (long long)g.batch * g.Hl, PFh, NW * RW) &&
+             encode_rows_map(&tmG, pl.guid, (long long)g.Wl * CG, (long long)g.batch * g.Hl, PGh, NW * RW + 1))
+                ? 1
+                : 0;
         // KB's predecessor: k2_tree / k2_slab_solve (they wait for KA before
         // triggering) or, with a single KA tile per band, KA itself
         const bool early = slab || PSA > 1;
         const int nwa_shift = (NWA & (NWA - 1)) == 0 ? __builtin_ctz((unsigned)NWA) : -1;
         TileOut to{pl.out, pl.transpose_out, pl.step, pl.nph, NWA, PSA, early ? 1 : 0, nwa_shift, pl.ratio,
-                   pl.ratio_floor, pl.und, stage_mode, tstore ? 1 : 0, 0, 0};
+                   pl.ratio_floor, pl.und, stage_mode, 0, 0};
         {
             // lean launch: staged by tensor maps, overlapping bands averaged by shuffles and stored
             // directly (the conditions of kb_tile's `direct`, all launch-uniform here), several chunks
@@ -2675,7 +2588,7 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
                 return v ? std::atoi(v) : 1;
             }();
             constexpr int DV = (RW * C) % 4 == 0 ? 4 : ((RW * C) % 2 == 0 ? 2 : 1);
-            const bool lean_ok = kb_has_lean(R, C) && lean_env && stage_mode == 2 && !tstore && g.P > 1 && pl.nph > 1 && g.tau <= 3 &&
+            const bool lean_ok = kb_has_lean(R, C) && lean_env && stage_mode != 0 && g.P > 1 && pl.nph > 1 && g.tau <= 3 &&
                                  !pl.ratio && pl.transpose_out && (C == 1 || DV == 4) &&
                                  ((long long)g.Hl * C) % DV == 0 && (g.img_stride % DV) == 0 &&
                                  (reinterpret_cast<uintptr_t>(pl.out) & (DV * 4 - 1)) == 0;
@@ -2702,7 +2615,7 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
         e = cudaFuncSetAttribute(kb_tile<R, C, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         e = launch_pdl(kb_tile<R, C, CG>, kgrid, dim3(32, NW), smem, st, g, pl.src, pl.guid, (const float*)pl.z,
-                       (const float*)pl.maps, to, pl.err, *pl.w, tmF, tmG, tmO);
+                       (const float*)pl.maps, to, pl.err, *pl.w, tmF, tmG);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
