@@ -1626,9 +1626,9 @@ struct TileOut {
     int ratio;
     float floor_;
     float* und;
-    // the CTA stages its input rows (image + guidance) in shared memory with one bulk
-    // (TMA) copy per row segment instead of per-lane loads (r >= 2, packed input,
-    // no row-slab neighbours, 16-byte aligned rows; decided on the host)
+    // the CTA stages its input rows (image + guidance) in shared memory with two tensor-map TMA
+    // boxes instead of per-lane loads (r >= 2, packed input, no row-slab neighbours, 16-byte
+    // aligned rows; decided on the host)
     int stage;
     // band tiles [lean_lo, lean_hi) run kb_lean (host: the launch-uniform conditions hold and the
     // tile is interior); empty range otherwise

@@ -24,6 +24,13 @@ CASES = [  # (h, w, c, r, tau, lam, T)
     (70, 64, 1, 1, 1, 900.0, 1),
     (90, 100, 1, 1, 2, 400.0, 2),
     (60, 100, 2, 2, 3, 400.0, 2),
+    # rows on 16-byte bounds in both orientations (TMA-staged KB where the schedule allows),
+    # several interior band tiles, r = 2 .. 4, a partial last row tile
+    (328, 400, 1, 2, 3, 400.0, 4),
+    (132, 260, 1, 2, 1, 300.0, 2),
+    (184, 100, 1, 3, 2, 900.0, 2),
+    (144, 80, 1, 4, 5, 100.0, 2),
+    (96, 264, 3, 2, 2, 400.0, 2),
     # tall lines: long reduced systems
     (4100, 40, 2, 1, 2, 400.0, 2),
     (9000, 36, 1, 1, 1, 900.0, 1),
