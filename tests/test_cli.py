@@ -19,6 +19,9 @@ HAVE_REF = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libsgwls_ref.so"
 
 
 def run(*args, env=None):
+    if not os.path.exists(EXE):  # normally built by __graft_entry__.build(); g++ only, no GPU needed
+        from paper_1705_01674_b200._build import build_cli
+        build_cli()
     assert os.path.exists(EXE), "run __graft_entry__.build() first"
     e = dict(os.environ)
     e.pop("SGWLS_THREADS", None)
