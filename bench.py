@@ -408,6 +408,7 @@ def e2e_leg(args, wl, cfg, world, rank, dist):
     err = N.errbuf()
     L = N.lib()
     steps = args.steps
+    self_guided = False
     if wl.sparse:
         per = max(1, wl.batch // world)
         trip = [WL.gen_c4(rank * per + i) for i in range(per)]
@@ -458,7 +459,11 @@ def e2e_leg(args, wl, cfg, world, rank, dist):
         el = float(tt.item())
     return {"value": world * px * steps / el / 1e6, "unit": "MPix/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": el / steps * 1e3,
-            "api": "sgwls_b200_interpolate_sparse_batch" if wl.sparse else "sgwls_b200_smooth (host pointers, pinned)"}
+            "api": "sgwls_b200_interpolate_sparse_batch" if wl.sparse else "sgwls_b200_smooth (host pointers, pinned)",
+            "inputs": ("values + mask + guidance per pair, pipelined over sub-batches inside the call" if wl.sparse
+                       else ("guidance = input: ONE host buffer passed as target and guidance "
+                             "(the reference's smooth(img, img, cfg)), uploaded once" if self_guided
+                             else "target and guidance buffers"))}
 
 
 def e2e_sharded(args, wl, sm, ht, hg, world):
