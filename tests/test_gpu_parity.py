@@ -316,3 +316,26 @@ def test_any_radius_sparse_and_pivot_error(port):
     gbad[20, 30] = np.nan
     with pytest.raises(S.Error, match="non-positive pivot"):
         S.smooth(vals, gbad, cfg)
+
+
+def test_random_shapes_on_the_staged_path(port):
+    """Seeded random r = 2 cases with rows on 16-byte bounds in both orientations: KB's TMA-staged
+    input (tensor-map boxes starting off the 16-byte grid, partial last row tiles, first / interior /
+    last band tiles, 1-3 channels, both first axes) against the oracle."""
+    rng = np.random.default_rng(20261021)
+    worst = 0.0
+    for i in range(14):
+        h = 4 * int(rng.integers(10, 120))
+        w = 4 * int(rng.integers(10, 130))
+        c = int(rng.integers(1, 4))
+        tau = int(rng.integers(1, 6))
+        T = int(rng.integers(1, 5))
+        axis = int(rng.integers(0, 2))
+        kind = int(rng.integers(0, 2))
+        t = _piecewise(rng, h, w, c)
+        g = _piecewise(rng, h, w, 1)
+        cfg = _cfg(float(rng.choice([50.0, 400.0, 900.0])), 2, tau, T, kind, axis)
+        err = float(np.abs(S.smooth(t, g, cfg).astype(np.float64) - port.smooth(t, g, cfg)).max())
+        worst = max(worst, err)
+        assert err <= TOL, f"case {i}: {h}x{w}x{c} tau={tau} T={T} axis={axis} kind={kind}: max|d|={err:.3g}"
+    print(f"staged random shapes: worst max|d| = {worst:.3g}")
