@@ -81,7 +81,7 @@ int sgwls_b200_validate(const sgwls_b200_config* cfg, char* err, size_t errlen);
 int sgwls_b200_smooth(const float* target, int width, int height, int channels, const float* guidance,
                       int guidance_channels, const sgwls_b200_config* cfg, float* out, char* err, size_t errlen);
 
-/* `batch` independent smooth calls (target i with guidance i).  Batches above ~8 MPix run as an
+/* `batch` independent smooth calls (target i with guidance i).  Larger batches run as an
  * upload / filter / download pipeline over sub-batches on three streams (fastest from pinned
  * host buffers); results and errors as `batch` serial calls (the first failing image decides). */
 int sgwls_b200_smooth_batch(const float* targets, const float* guidances, int batch, int width, int height,

@@ -121,8 +121,8 @@ def test_self_guided_call_uploads_once_same_result():
 
 
 def test_host_batch_pipeline_equals_single_calls():
-    """Host batches beyond ~8 MPix run as upload / filter / download stages over sub-batches
-    (6 images of 1 MPix: sub-batches of 5 + 1): bit-identical to the single calls"""
+    """Larger host batches run as upload / filter / download stages over sub-batches
+    (6 images of 1 MPix: three sub-batches of 2): bit-identical to the single calls"""
     cfg = S.SmoothConfig(lambda_=400.0, r=2, tau=2, weight=S.WeightParams(kind=S.WeightKind.Exp, sigma_r=0.05))
     t = np.stack([_scene(1024, 1024, 10 + i) for i in range(6)])
     g = np.stack([_scene(1024, 1024, 20 + i) for i in range(6)])
