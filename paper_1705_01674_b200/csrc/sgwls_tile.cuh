@@ -2526,8 +2526,9 @@ inline cudaError_t launch_tile_rcg(const PassLaunch& pl, cudaStream_t st) {
             return n == 4 || n == 8 || n == 16 || n == 32 ? n : 0;
         }();
         // measured on B200 (level 2 as a merge tree): 32 warps for the long
-        // reduced systems of r <= 2 (c5 +4 %), 16 from 16 super records on, 8 below (c1 +3 %)
-        int NG = ng_env ? ng_env : (PSA >= 128 && R <= 2 ? 32 : (PSA >= 20 ? 16 : 8));
+        // reduced systems of r <= 2 (c5, 256 super records: +4 %; c4, 86: K2 -8 %), 16 from 16 super
+        // records on, 8 below (c1 +3 %)
+        int NG = ng_env ? ng_env : (PSA >= 64 && R <= 2 ? 32 : (PSA >= 20 ? 16 : 8));
         if (R > 2 && NG > 16) NG = 16;  // 1024 threads hold only 64 registers
         while (NG > 4 && k2_tree_smem<R, C>(NG) > 200 * 1024) NG /= 2;
         // staging all the CTA's super-records in shared memory first (one latency)
